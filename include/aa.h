@@ -1,0 +1,158 @@
+/*
+ * aa.h — C ABI of libaa: the Anderson-acceleration hot path of
+ * Lockhart, Gardner, Woodward, Thomas, Olson, "Performance of Low
+ * Synchronization Orthogonalization Methods in Anderson Accelerated Fixed
+ * Point Solvers" (arXiv 2110.09667), built for NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n.
+ *
+ * One AA iteration (Alg. 1 l.3-7, with Alg. 2, inside):
+ *   f_i = G(x_i) - x_i;  Delta f_{i-1} = f_i - f_{i-1};  Delta g_{i-1} = G(x_i) - G(x_{i-1})
+ *   if the window is full: QRDelete (Givens)
+ *   QRAdd_{MGS | ICWY | CGS2 | DCGS2} (Algs. 3-6)
+ *   solve R gamma = Q^T f_i (Alg. 2 l.9)
+ *   x_{i+1} = G(x_i) - G_i gamma (Alg. 1 l.7)
+ * Every step runs in libaa's CUDA kernels; each global reduction of a
+ * distributed run is exactly one ncclAllReduce (sum, fp64) of an O(m)-word
+ * vector.  Numbers are IEEE fp64 throughout.
+ *
+ * CONVENTIONS
+ *  - Vector arguments named x*, gx*, v are DEVICE pointers to n_local fp64
+ *    values, 16-byte aligned (else AA_ERR_ARG).  The caller owns them; libaa
+ *    reads/writes them only inside the stream-ordered work of the call and
+ *    never retains them.  Output vectors may alias inputs of the same call
+ *    (every row is read before it is written).
+ *  - libaa owns Q, R, T, the Delta G window, f_{i-1}, G(x_{i-1}) and all
+ *    scratch: (2m+2) vectors of n_local (padded to a multiple of 256 rows) plus
+ *    O(m^2) words, allocated once in aa_create.
+ *  - aa_init / aa_step / aa_delete_oldest only ENQUEUE on the handle's stream
+ *    and return without a host synchronisation.  aa_stats synchronises.
+ *  - Host control flow depends only on (i, m_i, variant, options), all known
+ *    on the host; no device->host transfer happens per iteration.
+ *  - Errors: argument errors return immediately with no state change.  A CUDA
+ *    or NCCL failure makes the handle sticky-failed: every later call except
+ *    aa_stats / aa_destroy / aa_status_string returns the same error.
+ *  - Collective calls (nranks > 1): aa_create, aa_step, aa_delete_oldest,
+ *    aa_stats, aa_destroy must be called by every rank in the same order with
+ *    the same m / variant / options.  n_local may differ per rank (contiguous
+ *    row blocks).
+ *  - Handles are not thread-safe.  One handle per solve.
+ */
+#ifndef AA_H
+#define AA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aa_ctx* aa_handle_t;
+
+/* QRAdd variants (Algs. 3-6). */
+enum aa_variant {
+    AA_QR_MGS = 0,   /* Alg. 3: m_i dependent reductions per add (baseline)            */
+    AA_QR_ICWY = 1,  /* Alg. 4: inverse compact WY MGS, 2 reductions (+1 after delete)  */
+    AA_QR_CGS2 = 2,  /* Alg. 5: CGS with reorthogonalisation, 3 reductions              */
+    AA_QR_DCGS2 = 3  /* Alg. 6: delayed CGS-2, 2 reductions                             */
+};
+
+enum aa_status {
+    AA_OK = 0,
+    AA_ERR_ARG = 1,        /* bad pointer / size / option / call order                  */
+    AA_ERR_STATE = 2,      /* call not allowed in the current state                     */
+    AA_ERR_CUDA = 3,       /* CUDA runtime failure (sticky)                              */
+    AA_ERR_NCCL = 4,       /* NCCL failure or NCCL library unavailable (sticky)         */
+    AA_ERR_NOMEM = 5,      /* device allocation failed in aa_create                     */
+    AA_ERR_BREAKDOWN = 6   /* reported by aa_stats: a new column was (numerically)
+                              linearly dependent (R_kk <= eps_a ||Delta f||, reading A12) */
+};
+
+/* Options for aa_set_option (call after aa_create, before aa_init). */
+enum aa_option {
+    AA_OPT_DAMPING_BETA = 0,   /* beta in (0,1]; default 1 = Alg. 1 exactly.  beta != 1:
+                                  x_{i+1} = G(x_i) - G_i gamma - (1-beta)(f_i - Q Q^T f_i)
+                                  (not in the paper; reading A13)                */
+    AA_OPT_ICWY_DELETE = 1,    /* 0 = SEPARATE (paper: T update after QRDelete is its own
+                                  reduction; 3 allreduces per recycle iteration);
+                                  1 = MERGED into QRAdd's first reduction (2 allreduces)  */
+    AA_OPT_DCGS2_COND = 2,     /* reorthogonalise when m_i > val; paper: 3 (Alg. 6 l.2);
+                                  2 is the shape-allowed alternative (reading A2)          */
+    AA_OPT_DCGS2_RSCALE = 3,   /* 0 = R += s verbatim (Alg. 6 l.5); 1 = R += R_kk s (A3)  */
+    AA_OPT_BREAKDOWN_EPS = 4,  /* eps_a; default 10 * DBL_EPSILON * sqrt(n_global)        */
+    AA_OPT_PROFILE = 5,        /* 1 = record per-kernel CUDA events (aa_timings)           */
+    AA_OPT_N_GLOBAL = 6        /* global vector length (for the default eps_a)             */
+};
+
+/* aa_stats flags */
+#define AA_STATS_LOO 1     /* also compute ||I - Q^T Q||_F (one Gram pass + 1 allreduce) */
+#define AA_STATS_RESET 2   /* reset cumulative counters after reading                    */
+
+/* Ledger phases (logical synchronisations of the paper's counting). */
+enum aa_phase { AA_PH_QRADD = 0, AA_PH_QRDELETE = 1, AA_PH_LSP_RHS = 2, AA_PH_NORM = 3,
+                AA_PH_OTHER = 4 };
+
+struct aa_stats {
+    int64_t iter;              /* AA iterations done (Alg. 1 loop index i)                  */
+    int32_t m_i;               /* active window columns                                     */
+    int32_t sync_points_last;  /* global reduction points in the last aa_step              */
+    int32_t allreduce_last;    /* physical ncclAllReduce calls in the last aa_step (0 if p=1)*/
+    int32_t pad0;
+    int64_t allreduce_total;
+    int64_t logical_sync[5];   /* cumulative, by aa_phase (paper ledger)                    */
+    int64_t logical_sync_last[5];
+    double f_norm;             /* ||f_i||_2 of the last step (global)                       */
+    double dx_norm;            /* ||x_{i+1} - x_i||_2 of the last step (global)             */
+    double r_ratio_min;        /* min over the run of R_kk / ||Delta f|| (breakdown margin)  */
+    double loo;                /* ||I - Q^T Q||_F if AA_STATS_LOO, else -1                  */
+    int32_t breakdown;         /* sticky breakdown flag                                     */
+    int32_t pad1;
+};
+
+/* NCCL rendezvous: rank 0 calls this, broadcasts the 128 bytes (e.g. with
+ * torch.distributed), every rank passes them to aa_create.  Needs libnccl.so.2
+ * at run time (dlopen); AA_ERR_NCCL if unavailable. */
+int aa_comm_unique_id(void* id128);
+
+/* Create a solver for n_local local rows, window depth m (1 <= m <= 64), QRAdd
+ * variant (enum aa_variant).  nranks == 1: no communicator (id128 may be NULL).
+ * cuda_stream: the cudaStream_t every call enqueues on; NULL = the CUDA legacy
+ * default stream (so work is ordered with a caller that uses stream 0).
+ * Collective over the ranks when nranks > 1. */
+int aa_create(aa_handle_t* h, int64_t n_local, int m, int qr_variant, int rank, int nranks,
+              const void* id128, void* cuda_stream);
+int aa_set_option(aa_handle_t h, int opt, double val);
+
+/* Alg. 1 l.1: f_0 = G(x_0) - x_0, remember G(x_0) and f_0, x1_out = G(x_0).
+ * x1_out may alias gx0.  Resets the window. */
+int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out);
+
+/* One AA iteration (Alg. 1 l.3-7 with Alg. 2): given x_i and G(x_i) produce x_{i+1}.
+ * QRDelete is fused in automatically when the window is full (m_i == m). */
+int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next);
+
+/* Same computation with HOST buffers (pinned or pageable): copies in, runs aa_step,
+ * copies x_next back and synchronises.  For end-to-end measurement. */
+int aa_step_host(aa_handle_t h, const double* x_i_host, const double* gx_i_host,
+                 double* x_next_host);
+
+/* Stand-alone Givens QRDelete of the oldest window column:
+ * rotates Q and R, drops the oldest Delta G column; ICWY also rebuilds T with
+ * one reduction.  aa_step calls the fused form automatically. */
+int aa_delete_oldest(aa_handle_t h);
+
+/* Synchronises the stream and reports counters; see struct aa_stats.  Returns
+ * AA_ERR_BREAKDOWN if the sticky breakdown flag is set (stats still filled). */
+int aa_stats(aa_handle_t h, struct aa_stats* out, int flags);
+
+/* Empty the window (restart policy after a breakdown).  The next aa_step
+ * behaves like Alg. 2's i = 1 branch. */
+int aa_reset(aa_handle_t h);
+
+int aa_destroy(aa_handle_t h);
+const char* aa_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AA_H */

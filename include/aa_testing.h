@@ -1,0 +1,50 @@
+/*
+ * aa_testing.h — libaa hooks for tests and benchmarks (not part of the solver API).
+ * Same conventions as aa.h.
+ */
+#ifndef AA_TESTING_H
+#define AA_TESTING_H
+
+#include <stdint.h>
+#include "aa.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Append an arbitrary column v (device, n_local fp64) to the QR factorisation with
+ * the handle's QRAdd variant, exactly as aa_step appends Delta f (QRDelete first if
+ * the window is full), without touching x / G state.  Needed by the orthogonality
+ * stress test (config 5a): forming v as a difference of iterates would cancel. */
+int aa_test_qradd(aa_handle_t h, const double* v);
+
+/* Copy the replicated small factors to host memory (synchronises):
+ * R (m x m, column-major, only the leading m_i x m_i block is meaningful), T (m x m,
+ * column-major, ICWY only), gamma (m_i), scale (m: lazy 1/R_kk per Q slot). */
+int aa_get_small(aa_handle_t h, double* R, double* T, double* gamma, double* scale);
+
+/* Copy the normalised active Q columns (n_local x m_i, column-major, ld = n_local)
+ * to a device buffer (applies the lazy per-column scale).  Synchronises. */
+int aa_get_q(aa_handle_t h, double* q_out_dev);
+
+/* Per-class kernel timings (ms, accumulated since the last reset) when
+ * AA_OPT_PROFILE = 1.  Classes: 0 pass1 (K1), 1 project (K2), 2 update (K4),
+ * 3 allreduce, 4 whole aa_step.  counts[c] = number of events. Synchronises. */
+int aa_timings(aa_handle_t h, double* ms_out5, int64_t* counts5, int reset);
+
+/* Number of libaa kernels launched since the handle was created. */
+int64_t aa_kernel_launches(aa_handle_t h);
+
+/* Counter-based SplitMix64 uniform generator on the device:
+ * out[i] = lo + (hi - lo) * u(seed + stream * 2^48 + offset + i), u in [0, 1),
+ * computed with __dmul_rn / __dadd_rn so it is bitwise equal to aa_inputs.uniform. */
+int aa_fill_uniform(double* out_dev, int64_t n, int64_t offset, uint64_t seed, uint64_t stream,
+                    double lo, double hi, void* cuda_stream);
+
+/* Build-time facts: sm target, tile rows, stages, block size (for the report). */
+int aa_build_info(char* buf, int len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,212 @@
+// aa_device.cuh — libaa device-side data structures, PTX wrappers (TMA bulk copy,
+// mbarrier, fp64 DMMA) and the O(m^2) small-factor routines (K3) of the AA hot
+// path of arXiv 2110.09667.  P:n = PAPER.md line n.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aa {
+
+constexpr int MMAX = 64;                 // largest window depth m
+constexpr int NT = 256;                  // threads per CTA (8 warps)
+constexpr int NWARP = NT / 32;
+constexpr int NIN_MAX = 2 * MMAX + 4;    // input column streams of one kernel
+constexpr int LRED = 2304;               // words per reduction slot (>= 4+3*63+63*62/2)
+constexpr int NSLOT = MMAX + 2;          // reduction slots per iteration
+constexpr int PB_COLS_PER_WARP = 9;      // ceil((MMAX+2)/NWARP)
+
+enum Op : int {
+  OP_K1 = 0,        // prologue (Delta f / Delta g) + streaming Givens + block multi-dot
+  OP_K2_ICWY = 1,   // Alg. 4 l.5: Delta f - Q T^{-1} r, norms
+  OP_K2_DCGS2 = 2,  // Alg. 6 l.4 + l.7: delayed reorthogonalisation + projection, norms
+  OP_K2A_CGS2 = 3,  // Alg. 5 l.2-3: y = Delta f - Q s, z = Q^T y
+  OP_K2B_CGS2 = 4,  // Alg. 5 l.4: Delta f = y - Q z, norms
+  OP_K2_MGS = 5,    // Alg. 3 l.3 + next l.2: one axpy + one dot (or the norm)
+  OP_K4 = 6,        // Alg. 2 l.9 + Alg. 1 l.7: gamma, x_{i+1} = G(x_i) - G_i gamma; commit
+  OP_GRAM = 7       // diagnostic: lower triangle of Q^T Q (loss of orthogonality)
+};
+
+enum Variant : int { V_MGS = 0, V_ICWY = 1, V_CGS2 = 2, V_DCGS2 = 3 };
+
+enum Flags : int {
+  F_EXT_DF = 1,       // K1: the new column is caller-provided (aa_test_qradd)
+  F_DELETE_ONLY = 2,  // K1/K4: stand-alone QRDelete (aa_delete_oldest)
+  F_COMMIT_ONLY = 4   // K4: no rows, only the small-factor commit
+};
+
+// Replicated small factors (identical on every rank: every rank recomputes them
+// from the same allreduce results).  Written only by the last CTA of a kernel.
+struct SmallState {
+  double R[MMAX * MMAX];     // column-major, leading dim MMAX
+  double T[MMAX * MMAX];     // ICWY: I + L (reading A5), column-major
+  double scale[MMAX];        // lazy normalisation: Q_j(true) = scale[j] * Q_j(stored)
+  double gamma[MMAX];
+  double dx2_local;          // this rank's ||x_{i+1} - x_i||^2 from the last update
+  double f2;                 // ||f_i||^2 (global) of the last step
+  double rratio_min;         // min R_kk / ||Delta f||
+  double last_rkk;
+  int breakdown;             // sticky
+  unsigned int counter;      // cross-CTA arrival ticket
+};
+
+// K1 reduction-slot layout (words), identical on host and device.
+struct K1Layout {
+  int off_df, off_f, off_x, n_x, off_gram, n_gram, words;
+  __host__ __device__ static K1Layout make(int k, bool has_x, bool has_gram) {
+    K1Layout L;
+    L.off_df = 4;
+    L.off_f = 4 + k;
+    L.off_x = 4 + 2 * k;
+    L.n_x = (has_x && k >= 2) ? k - 1 : 0;
+    L.off_gram = L.off_x + L.n_x;
+    L.n_gram = (has_gram && k >= 3) ? (k - 1) * (k - 2) / 2 : 0;
+    L.words = L.off_gram + L.n_gram;
+    return L;
+  }
+};
+
+struct KParams {
+  int op, variant, flags;
+  int m;            // window capacity
+  int k;            // existing columns after QRDelete (new column index)
+  int c_in;         // K1: Q columns read (m at recycle, k at start-up); GRAM: columns
+  int recycle;      // QRDelete fused into this step
+  int has_x;        // K1: Q_{0:k-2}^T q_{k-1} needed (ICWY T row / DCGS-2 s)
+  int gram;         // 0 none, 1 strict lower k x k (ICWY after delete), 2 lower incl. diag
+  int reortho;      // DCGS-2 delayed reorthogonalisation active this step
+  int rscale;       // DCGS-2 R update reading A3
+  int icwy_merged;  // (informational; layout is the same)
+  int mgs_j;        // MGS pass index j (1..k)
+  int final_slot;   // reduction slot holding (||v'||^2, v'^T f)
+  int red_slot;     // slot this kernel writes
+  int words;        // words this kernel reduces
+  int nin, tr, str, stages;
+  int beta_on;
+  long long n;      // local rows
+  double beta, eps_a;
+  const double* in[NIN_MAX];
+  unsigned long long exact[3];   // bit i: input i is a caller buffer (exactly n rows)
+  double* Q;        // Q base (column j at Q + j*ld)
+  long long ld;
+  double* fp;       // f_{i-1} -> f_i
+  double* gp;       // G(x_{i-1}) -> G(x_i)
+  double* dg_out;   // Delta G ring slot written by K1
+  double* x_out;    // K4 output
+  SmallState* st;
+  double* red;      // reduction slots (slot s at red + s*LRED)
+  double* part;     // per-CTA partials (CTA b at part + b*LRED)
+};
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col)
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ K3: small factors
+// All routines run on ONE warp (lanes cooperate over columns / rows) with operands
+// in shared memory, leading dimension MMAX, and end with __syncwarp().
+
+// QRDelete on R (reading A7): drop column 0 of the mold x mold
+// factor, re-triangularise the upper-Hessenberg remainder with mold-1 Givens
+// rotations of adjacent rows, rho = hypot(a,b) >= 0.  Output Rw ((mold-1)^2, col-major
+// MMAX) and the rotation coefficients cs/sn (applied to Q's columns by K1).
+__device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double* cs, double* sn) {
+  const int lane = threadIdx.x & 31;
+  const int nc = mold - 1;  // columns of the Hessenberg matrix
+  for (int idx = lane; idx < mold * nc; idx += 32) {
+    int i = idx % mold, j = idx / mold;
+    Rw[i + j * MMAX] = (i <= j + 1) ? Rg[i + (j + 1) * MMAX] : 0.0;
+  }
+  __syncwarp();
+  for (int j = 0; j < nc; ++j) {
+    const double a = Rw[j + j * MMAX], b = Rw[j + 1 + j * MMAX];
+    const double rho = hypot(a, b);
+    const double c = rho > 0.0 ? a / rho : 1.0;
+    const double s = rho > 0.0 ? b / rho : 0.0;
+    for (int l = j + 1 + lane; l < nc; l += 32) {
+      const double h1 = Rw[j + l * MMAX], h2 = Rw[j + 1 + l * MMAX];
+      Rw[j + l * MMAX] = __dadd_rn(__dmul_rn(c, h1), __dmul_rn(s, h2));
+      Rw[j + 1 + l * MMAX] = __dadd_rn(__dmul_rn(-s, h1), __dmul_rn(c, h2));
+    }
+    __syncwarp();
+    if (lane == 0) {
+      Rw[j + j * MMAX] = rho;
+      Rw[j + 1 + j * MMAX] = 0.0;
+      cs[j] = c;
+      sn[j] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// Forward substitution with a unit lower-triangular T (Alg. 4 l.4 "T^{-1} R"; A5):
+// r <- T^{-1} r in place, r has k entries in shared memory.
+__device__ void k3_forward_unit_lower(const double* T, double* r, int k) {
+  const int lane = threadIdx.x & 31;
+  for (int l = 0; l < k; ++l) {
+    __syncwarp();
+    const double rl = r[l];
+    for (int j = l + 1 + lane; j < k; j += 32) r[j] -= T[j + l * MMAX] * rl;
+  }
+  __syncwarp();
+}
+
+// Back substitution R gamma = c (Alg. 2 l.9), R upper triangular K x K; c overwritten.
+__device__ void k3_back_subst(const double* R, double* c, double* gamma, int K) {
+  const int lane = threadIdx.x & 31;
+  for (int j = K - 1; j >= 0; --j) {
+    __syncwarp();
+    const double gj = c[j] / R[j + j * MMAX];
+    if (lane == 0) gamma[j] = gj;
+    for (int i = lane; i < j; i += 32) c[i] -= R[i + j * MMAX] * gj;
+  }
+  __syncwarp();
+}
+
+}  // namespace aa

@@ -1,0 +1,728 @@
+// aa_kernels.cuh — the streaming kernels of libaa (sm_100a).
+//
+// One templated persistent kernel per op.  Every op is a pass over row tiles of
+// TR rows: a single thread issues TMA 1-D bulk copies (cp.async.bulk, completion on
+// an mbarrier) of the op's input columns for the tile into a ring of shared-memory
+// stages; all threads then run the op's row-wise work (phase A) out of shared memory
+// and, where the op needs many dot products, a block multi-dot over the staged tile
+// (phase B: lane = row, warp = column set, or fp64 DMMA for Gram blocks).  Per-CTA
+// partial sums are reduced across CTAs in a fixed order by the last CTA to finish
+// (deterministic), which also commits the replicated small factors.
+//
+// Small-factor work (K3: Givens on R, T^{-1}, back-substitution) is recomputed at the
+// head of every CTA from the replicated state and the latest allreduce results, so no
+// extra launch and no device->host copy is needed between reductions.
+#pragma once
+#include "aa_device.cuh"
+
+namespace aa {
+
+constexpr int MAXSTAGES = 8;
+
+struct HeadArea {
+  double coef[NIN_MAX];
+  double coef2[MMAX + 2];
+  double sc[NIN_MAX];
+  double cs[MMAX];
+  double sn[MMAX];
+  double scal[8];
+  double redw[NWARP][4];
+  int lcol[MMAX + 2];
+  int rcol[4];
+  int na, nr, is_last, pad;
+};
+
+__host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+__host__ __device__ constexpr size_t head_bytes() { return align_up(sizeof(HeadArea), 128); }
+__host__ __device__ constexpr size_t bar_bytes() { return 128; }
+// scratch for the head / commit (aliases the stage ring before and after the pipeline)
+__host__ __device__ constexpr size_t scratch_bytes() { return (2 * MMAX * MMAX + 4 * MMAX) * sizeof(double); }
+
+__device__ __forceinline__ double cur_scale(const KParams& p, int j) {
+  // scale of stored Q column j as seen after this step's K1: rotated columns (QRDelete)
+  // were written as true values.
+  return p.recycle ? 1.0 : p.st->scale[j];
+}
+
+// ---------------------------------------------------------------------------- heads
+// Assemble ICWY's T' (k x k unit lower) into Tw: rows 0..k-2 from the stored T
+// (start-up) or the post-delete Gram (recycle / delete-only), row k-1 from Alg. 4 l.1.
+__device__ void icwy_assemble_T(const KParams& p, const double* red0, double* Tw, int k) {
+  const int lane = threadIdx.x & 31;
+  const K1Layout L = K1Layout::make(k, true, p.gram != 0);
+  for (int idx = lane; idx < k * k; idx += 32) {
+    const int i = idx % k, j = idx / k;
+    double v;
+    if (i == j) v = 1.0;
+    else if (j > i) v = 0.0;
+    else if (p.flags & F_DELETE_ONLY) v = red0[i * (i - 1) / 2 + j];
+    else if (i == k - 1) v = red0[L.off_x + j];
+    else if (p.recycle) v = red0[L.off_gram + i * (i - 1) / 2 + j];
+    else v = p.st->T[i + j * MMAX];
+    Tw[i + j * MMAX] = v;
+  }
+  __syncwarp();
+}
+
+struct K4Head {
+  int K;          // columns of the updated factor
+  double rkk, df2;
+};
+
+// Everything Alg. 2 does after the reductions: the new R column per variant, R_kk,
+// Q^T f_i (merged into the existing reductions; A14), gamma by
+// back-substitution.  Writes Rw (K x K), Tw (ICWY), gamma/coef into H, c into cvec.
+__device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  double* Rw = scratch;
+  double* Tw = scratch + MMAX * MMAX;
+  double* v1 = Tw + MMAX * MMAX;  // MMAX words
+  double* cvec = v1 + MMAX;       // MMAX
+  double* cvec2 = cvec + MMAX;    // MMAX
+  const double* red0 = p.red;
+  const int k = p.k;
+  K4Head out{};
+  const int mold = k + 1;
+  if (p.recycle) {
+    k3_givens_delete(p.st->R, mold, Rw, H.cs, H.sn);
+  } else {
+    for (int idx = lane; idx < k * k; idx += 32) {
+      const int i = idx % k, j = idx / k;
+      Rw[i + j * MMAX] = p.st->R[i + j * MMAX];
+    }
+    __syncwarp();
+  }
+  if (p.flags & F_DELETE_ONLY) {
+    if (p.variant == V_ICWY) icwy_assemble_T(p, red0, Tw, k);
+    out.K = k;
+    return out;
+  }
+  const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
+  const double* fin = p.red + p.final_slot * LRED;
+  const double vv = (k == 0) ? red0[1] : fin[0];
+  const double vf = (k == 0) ? red0[3] : fin[1];
+  const double rkk = sqrt(vv);
+  // new R column (rows 0..k-1 of column k)
+  if (p.variant == V_ICWY && k >= 1) {
+    icwy_assemble_T(p, red0, Tw, k);
+    for (int j = lane; j < k; j += 32) v1[j] = red0[L.off_df + j];
+    __syncwarp();
+    k3_forward_unit_lower(Tw, v1, k);
+    for (int j = lane; j < k; j += 32) Rw[j + k * MMAX] = v1[j];
+  } else {
+    for (int j = lane; j < k; j += 32) {
+      double r;
+      if (p.variant == V_MGS) r = (j == 0) ? red0[L.off_df] : p.red[j * LRED];
+      else if (p.variant == V_CGS2) r = red0[L.off_df + j] + p.red[LRED + j];   // s + z (Alg. 5 l.5)
+      else r = red0[L.off_df + j];                                               // DCGS-2 l.1 (A4)
+      Rw[j + k * MMAX] = r;
+    }
+  }
+  __syncwarp();
+  if (p.variant == V_DCGS2 && p.reortho) {  // Alg. 6 l.5 (verbatim R += s, or A3)
+    const double rk1 = Rw[(k - 1) + (k - 1) * MMAX];
+    for (int j = lane; j < k - 1; j += 32) {
+      const double s = red0[L.off_x + j];
+      Rw[j + (k - 1) * MMAX] += p.rscale ? rk1 * s : s;
+    }
+  }
+  if (lane == 0) {
+    Rw[k + k * MMAX] = rkk;
+    for (int i = 0; i < k; ++i) Rw[k + i * MMAX] = 0.0;
+  }
+  // c = Q^T f_i with the final Q
+  for (int j = lane; j < k; j += 32) cvec[j] = red0[L.off_f + j];
+  __syncwarp();
+  if (p.variant == V_DCGS2 && p.reortho && lane == 0) {
+    double acc = cvec[k - 1];
+    for (int j = 0; j < k - 1; ++j) acc -= red0[L.off_x + j] * cvec[j];
+    cvec[k - 1] = acc;
+  }
+  if (lane == 0) cvec[k] = vf / rkk;
+  __syncwarp();
+  for (int j = lane; j <= k; j += 32) cvec2[j] = cvec[j];
+  __syncwarp();
+  k3_back_subst(Rw, cvec2, H.coef, k + 1);  // gamma -> H.coef[0..k]
+  if (p.beta_on) {
+    for (int j = lane; j <= k; j += 32) {
+      double fs;
+      if (j == k) fs = 1.0 / rkk;
+      else if (p.variant == V_DCGS2 && p.reortho && j == k - 1) fs = 1.0;
+      else fs = cur_scale(p, j);
+      H.coef2[j] = cvec[j] * fs;
+    }
+    if (lane == 0) H.scal[0] = 1.0 - p.beta;
+  }
+  __syncwarp();
+  out.K = k + 1;
+  out.rkk = rkk;
+  out.df2 = red0[1];
+  return out;
+}
+
+template <int OP>
+__device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const double* red0 = p.red;
+  const int k = p.k;
+  if constexpr (OP == OP_K1) {
+    if (p.recycle) k3_givens_delete(p.st->R, p.c_in, scratch, H.cs, H.sn);
+    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->scale[j];
+    if (lane == 0) {
+      const int qb = (p.flags & F_DELETE_ONLY) ? 0 : 4;
+      if (p.flags & F_DELETE_ONLY) {
+        H.na = 0;
+        H.nr = 0;
+      } else {
+        H.na = k + 2;
+        for (int a = 0; a < k; ++a) H.lcol[a] = qb + a;
+        H.lcol[k] = 0;       // f_i
+        H.lcol[k + 1] = 1;   // Delta f
+        H.nr = 3;
+        H.rcol[0] = 1;
+        H.rcol[1] = 0;
+        H.rcol[2] = (k >= 1) ? qb + k - 1 : 0;
+      }
+    }
+  } else if constexpr (OP == OP_K2_ICWY) {
+    double* Tw = scratch;
+    double* v1 = scratch + MMAX * MMAX;
+    const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
+    icwy_assemble_T(p, red0, Tw, k);
+    for (int j = lane; j < k; j += 32) v1[j] = red0[L.off_df + j];
+    __syncwarp();
+    k3_forward_unit_lower(Tw, v1, k);   // Alg. 4 l.4
+    for (int j = lane; j < k; j += 32) H.coef[j] = v1[j] * cur_scale(p, j);
+  } else if constexpr (OP == OP_K2_DCGS2) {
+    const K1Layout L = K1Layout::make(k, p.has_x, false);
+    for (int j = lane; j < k; j += 32) {
+      const double sc = cur_scale(p, j);
+      H.sc[j] = sc;
+      H.coef[j] = (j < k - 1) ? red0[L.off_df + j] * sc : red0[L.off_df + j];
+      if (p.reortho && j < k - 1) H.coef2[j] = red0[L.off_x + j] * sc;
+    }
+  } else if constexpr (OP == OP_K2A_CGS2) {
+    const K1Layout L = K1Layout::make(k, false, false);
+    for (int j = lane; j < k; j += 32) {
+      const double sc = cur_scale(p, j);
+      H.sc[j] = sc;
+      H.coef[j] = red0[L.off_df + j] * sc;
+    }
+    if (lane == 0) {
+      H.na = k;
+      for (int a = 0; a < k; ++a) H.lcol[a] = a;
+      H.nr = 1;
+      H.rcol[0] = k;
+    }
+  } else if constexpr (OP == OP_K2B_CGS2) {
+    for (int j = lane; j < k; j += 32) H.coef[j] = p.red[LRED + j] * cur_scale(p, j);
+  } else if constexpr (OP == OP_K2_MGS) {
+    if (lane == 0) {
+      const int j = p.mgs_j;
+      const K1Layout L = K1Layout::make(k, false, false);
+      const double r = (j == 1) ? red0[L.off_df] : p.red[(j - 1) * LRED];
+      H.scal[0] = r * cur_scale(p, j - 1);
+      H.scal[1] = (j < k) ? cur_scale(p, j) : 1.0;
+    }
+  } else if constexpr (OP == OP_K4) {
+    k4_head(p, H, scratch);
+  } else if constexpr (OP == OP_GRAM) {
+    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->scale[j];
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------- producer
+__device__ __forceinline__ bool is_exact(const KParams& p, int i) {
+  return (p.exact[i >> 6] >> (i & 63)) & 1ull;
+}
+
+__device__ void issue_tile(const KParams& p, double* stage, uint64_t* bar, long long row0, int rows) {
+  uint32_t total = 0;
+  for (int i = 0; i < p.nin; ++i) {
+    uint32_t b = is_exact(p, i) ? ((uint32_t)rows * 8u) & ~15u : (uint32_t)align_up((size_t)rows * 8u, 16);
+    total += b;
+  }
+  mbar_arrive_expect_tx(bar, total);
+  for (int i = 0; i < p.nin; ++i) {
+    uint32_t b = is_exact(p, i) ? ((uint32_t)rows * 8u) & ~15u : (uint32_t)align_up((size_t)rows * 8u, 16);
+    if (b) bulk_g2s(stage + (size_t)i * p.str, p.in[i] + row0, b, bar);
+  }
+}
+
+// value of input column i at tile row r (falls back to a plain load for the odd last
+// row of a caller buffer that the 16-byte-granular bulk copy could not cover)
+__device__ __forceinline__ double ldS(const KParams& p, const double* S, int i, int r, int rows,
+                                      long long grow) {
+  if ((rows & 1) && r == rows - 1 && is_exact(p, i)) return p.in[i][grow];
+  return S[(size_t)i * p.str + r];
+}
+
+// ---------------------------------------------------------------------------- kernel
+template <int OP>
+__global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + head_bytes());
+  double* stage0 = reinterpret_cast<double*>(smem_raw + head_bytes() + bar_bytes());
+  double* scratch = stage0;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long n = p.n;
+  const int TR = p.tr, STR = p.str, NS = p.stages;
+  const size_t stage_words = (size_t)p.nin * STR;
+  const long long ntiles = (n + TR - 1) / TR;
+  const int k = p.k;
+
+  if (warp == 0) op_head<OP>(p, H, scratch);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const long long my_count =
+      (ntiles > (long long)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (tid == 0) {
+    fence_proxy_async();
+    for (int s = 0; s < NS && s < my_count; ++s) {
+      const long long t = blockIdx.x + (long long)s * gridDim.x;
+      const long long r0 = t * TR;
+      issue_tile(p, stage0 + s * stage_words, &bars[s], r0, (int)min((long long)TR, n - r0));
+    }
+  }
+
+  // phase-A accumulators (row-wise dots / norms)
+  double a0 = 0.0, a1 = 0.0;
+  // phase-B accumulators (block multi-dot): warp's columns x up to 3 right-hand sides
+  constexpr int NRB = (OP == OP_K1) ? 3 : (OP == OP_K2A_CGS2 ? 1 : 0);
+  constexpr int NCB = (NRB > 0) ? PB_COLS_PER_WARP : 1;
+  double acc[NCB][NRB > 0 ? NRB : 1];
+#pragma unroll
+  for (int c = 0; c < NCB; ++c)
+#pragma unroll
+    for (int b = 0; b < (NRB > 0 ? NRB : 1); ++b) acc[c][b] = 0.0;
+  // Gram accumulators (fp64 DMMA 8x8 blocks): up to 5 blocks per warp
+  constexpr bool HAS_GRAM = (OP == OP_K1 || OP == OP_GRAM);
+  constexpr int GB = HAS_GRAM ? 5 : 1;
+  double gc0[GB], gc1[GB];
+#pragma unroll
+  for (int g = 0; g < GB; ++g) gc0[g] = gc1[g] = 0.0;
+  const int kg = (OP == OP_GRAM) ? p.c_in : ((p.flags & F_DELETE_ONLY) ? p.c_in - 1 : k);
+  const int gbase = (OP == OP_GRAM || (p.flags & F_DELETE_ONLY)) ? 0 : 4;
+  const int nb8 = (kg + 7) / 8;
+  const int nblk = nb8 * (nb8 + 1) / 2;
+  const bool do_gram = HAS_GRAM && p.gram != 0 && (OP == OP_GRAM ? kg >= 1 : kg >= 2);
+  int gI[GB], gJ[GB];
+#pragma unroll
+  for (int g = 0; g < GB; ++g) {
+    const int blk = warp + g * NWARP;
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= blk) ++I;
+    gI[g] = I;
+    gJ[g] = blk - I * (I + 1) / 2;
+  }
+
+  for (long long it = 0; it < my_count; ++it) {
+    const int sidx = (int)(it % NS);
+    const uint32_t par = (uint32_t)((it / NS) & 1);
+    const long long tile = blockIdx.x + it * gridDim.x;
+    const long long row0 = tile * TR;
+    const int rows = (int)min((long long)TR, n - row0);
+    double* S = stage0 + sidx * stage_words;
+    mbar_wait(&bars[sidx], par);
+
+    // ------------------------------------------------------------ phase A (row-wise)
+    const int r = tid;
+    if (r < TR) {
+      const long long grow = row0 + r;
+      if constexpr (OP == OP_K1) {
+        const bool del_only = p.flags & F_DELETE_ONLY;
+        const int qb = del_only ? 0 : 4;
+        const int ncols = del_only ? p.c_in : (p.recycle ? p.c_in : k);
+        if (r < rows) {
+          double f = 0.0, df = 0.0;
+          if (!del_only) {
+            if (p.flags & F_EXT_DF) {
+              df = ldS(p, S, 0, r, rows, grow);
+              f = df;
+            } else {
+              // Alg. 1 l.3-5: f_i = G(x_i) - x_i, Delta f = f_i - f_{i-1}, Delta g = G(x_i) - G(x_{i-1})
+              const double x = ldS(p, S, 0, r, rows, grow);
+              const double g = ldS(p, S, 1, r, rows, grow);
+              const double fpv = S[2 * (size_t)STR + r];
+              const double gpv = S[3 * (size_t)STR + r];
+              f = g - x;
+              df = f - fpv;
+              const double dg = g - gpv;
+              p.fp[grow] = f;
+              p.gp[grow] = g;
+              p.dg_out[grow] = dg;
+            }
+          }
+          if (p.recycle) {
+            // QRDelete on Q: streaming carry form of the m-1 Givens rotations of adjacent
+            // column pairs; the last carry is the dropped column.
+            double carry = S[(size_t)qb * STR + r] * H.sc[0];
+            for (int j = 0; j < p.c_in - 1; ++j) {
+              const double qn = S[(size_t)(qb + j + 1) * STR + r] * H.sc[j + 1];
+              const double c = H.cs[j], s = H.sn[j];
+              const double out = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s, qn));
+              carry = __dadd_rn(__dmul_rn(-s, carry), __dmul_rn(c, qn));
+              S[(size_t)(qb + j) * STR + r] = out;
+              p.Q[(size_t)j * p.ld + grow] = out;
+            }
+          } else {
+            for (int j = 0; j < ncols; ++j) S[(size_t)(qb + j) * STR + r] *= H.sc[j];
+          }
+          if (!del_only) {
+            p.Q[(size_t)k * p.ld + grow] = df;  // unnormalised new column (lazy scale)
+            S[r] = f;
+            S[(size_t)STR + r] = df;
+          }
+        } else {
+          if (!del_only) {
+            S[r] = 0.0;
+            S[(size_t)STR + r] = 0.0;
+          }
+          for (int j = 0; j < ncols; ++j) S[(size_t)(qb + j) * STR + r] = 0.0;
+        }
+      } else if constexpr (OP == OP_K2_ICWY || OP == OP_K2B_CGS2) {
+        // ICWY: Alg. 4 l.5  Delta f - Q (T^{-1} r);  CGS-2: Alg. 5 l.4  y - Q z
+        if (r < rows) {
+          double v = S[(size_t)k * STR + r];
+#pragma unroll 4
+          for (int j = 0; j < k; ++j) v -= H.coef[j] * S[(size_t)j * STR + r];
+          p.Q[(size_t)k * p.ld + grow] = v;
+          a0 += v * v;
+          a1 += v * S[(size_t)(k + 1) * STR + r];
+        }
+      } else if constexpr (OP == OP_K2_DCGS2) {
+        if (r < rows) {
+          // Alg. 6 l.4 (reading A1): q_{k-1} <- q_{k-1} - Q_{0:k-2} s
+          double qn = S[(size_t)(k - 1) * STR + r] * H.sc[k - 1];
+          if (p.reortho) {
+#pragma unroll 4
+            for (int j = 0; j < k - 1; ++j) qn -= H.coef2[j] * S[(size_t)j * STR + r];
+            p.Q[(size_t)(k - 1) * p.ld + grow] = qn;
+          }
+          // Alg. 6 l.7: Delta f <- Delta f - Q_{0:k-1} R_{0:k-1,k}
+          double v = S[(size_t)k * STR + r];
+#pragma unroll 4
+          for (int j = 0; j < k - 1; ++j) v -= H.coef[j] * S[(size_t)j * STR + r];
+          v -= H.coef[k - 1] * qn;
+          p.Q[(size_t)k * p.ld + grow] = v;
+          a0 += v * v;
+          a1 += v * S[(size_t)(k + 1) * STR + r];
+        }
+      } else if constexpr (OP == OP_K2A_CGS2) {
+        if (r < rows) {
+          double v = S[(size_t)k * STR + r];
+#pragma unroll 4
+          for (int j = 0; j < k; ++j) v -= H.coef[j] * S[(size_t)j * STR + r];
+          p.Q[(size_t)k * p.ld + grow] = v;  // y (Alg. 5 l.2), in place
+          S[(size_t)k * STR + r] = v;
+          for (int j = 0; j < k; ++j) S[(size_t)j * STR + r] *= H.sc[j];
+        } else {
+          for (int j = 0; j <= k; ++j) S[(size_t)j * STR + r] = 0.0;
+        }
+      } else if constexpr (OP == OP_K2_MGS) {
+        if (r < rows) {
+          // Alg. 3 l.3 (column j-1) then l.2 for column j (or the norm, l.5)
+          double v = S[(size_t)STR + r] - H.scal[0] * S[r];
+          p.Q[(size_t)k * p.ld + grow] = v;
+          const double w = S[2 * (size_t)STR + r];
+          if (p.mgs_j < k) {
+            a0 += w * H.scal[1] * v;
+          } else {
+            a0 += v * v;
+            a1 += v * w;
+          }
+        }
+      } else if constexpr (OP == OP_K4) {
+        if (r < rows) {
+          // Alg. 1 l.7: x_{i+1} = G(x_i) - G_i gamma   [- (1-beta)(f_i - Q Q^T f_i), A13]
+          const double g = ldS(p, S, 0, r, rows, grow);
+          const double x = ldS(p, S, 1, r, rows, grow);
+          double xn = g;
+#pragma unroll 4
+          for (int j = 0; j <= k; ++j) xn -= H.coef[j] * S[(size_t)(2 + j) * STR + r];
+          if (p.beta_on) {
+            const int kf = k + 3;
+            double t = S[(size_t)kf * STR + r];
+            for (int j = 0; j <= k; ++j) t -= H.coef2[j] * S[(size_t)(kf + 1 + j) * STR + r];
+            xn -= H.scal[0] * t;
+          }
+          p.x_out[grow] = xn;
+          const double d = xn - x;
+          a0 += d * d;
+        }
+      } else if constexpr (OP == OP_GRAM) {
+        for (int j = 0; j < p.c_in; ++j) {
+          double& s = S[(size_t)j * STR + r];
+          s = (r < rows) ? s * H.sc[j] : 0.0;
+        }
+      }
+    }
+
+    // ------------------------------------------------------------ phase B (multi-dot)
+    if constexpr (NRB > 0 || HAS_GRAM) {
+      __syncthreads();
+      if constexpr (NRB > 0) {
+        const int na = H.na, nr = H.nr;
+        if (na > 0) {
+          for (int rr = lane; rr < TR; rr += 32) {
+            double rhs[NRB];
+#pragma unroll
+            for (int b = 0; b < NRB; ++b) rhs[b] = (b < nr) ? S[(size_t)H.rcol[b] * STR + rr] : 0.0;
+#pragma unroll
+            for (int c = 0; c < NCB; ++c) {
+              const int a = warp + c * NWARP;
+              if (a < na) {
+                const double v = S[(size_t)H.lcol[a] * STR + rr];
+#pragma unroll
+                for (int b = 0; b < NRB; ++b) acc[c][b] += v * rhs[b];
+              }
+            }
+          }
+        }
+      }
+      if constexpr (HAS_GRAM) {
+        if (do_gram) {
+          const int g_r = lane >> 2, g_c = lane & 3;
+          for (int r0 = 0; r0 < TR; r0 += 4) {
+#pragma unroll
+            for (int g = 0; g < GB; ++g) {
+              const int blk = warp + g * NWARP;
+              if (blk < nblk) {
+                const int ca = 8 * gI[g] + g_r, cb = 8 * gJ[g] + g_r;
+                const double av = (ca < kg) ? S[(size_t)(gbase + ca) * STR + r0 + g_c] : 0.0;
+                const double bv = (cb < kg) ? S[(size_t)(gbase + cb) * STR + r0 + g_c] : 0.0;
+                dmma_8x8x4(gc0[g], gc1[g], av, bv);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && it + NS < my_count) {
+      fence_proxy_async();
+      const long long t2 = blockIdx.x + (it + NS) * gridDim.x;
+      const long long r2 = t2 * TR;
+      issue_tile(p, S, &bars[sidx], r2, (int)min((long long)TR, n - r2));
+    }
+  }
+
+  // ------------------------------------------------------------ per-CTA partials
+  double* mypart = p.part + (size_t)blockIdx.x * LRED;
+  if constexpr (OP == OP_K1) {
+    const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
+    const bool del_only = p.flags & F_DELETE_ONLY;
+    if (!del_only) {
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) {
+        const int a = warp + c * NWARP;
+        if (a < H.na) {
+#pragma unroll
+          for (int b = 0; b < NRB; ++b) {
+            const double v = warp_sum(acc[c][b]);
+            if (lane == 0) {
+              int w = -1;
+              if (a < k) {
+                if (b == 0) w = L.off_df + a;
+                else if (b == 1) w = L.off_f + a;
+                else if (p.has_x && p.gram == 0 && a < k - 1) w = L.off_x + a;
+              } else if (a == k) {
+                if (b == 1) w = 0;  // f.f
+              } else {
+                if (b == 0) w = 1;       // df.df
+                else if (b == 1) w = 3;  // df.f
+              }
+              if (w >= 0) mypart[w] = v;
+            }
+          }
+        }
+      }
+      if (tid == 0) mypart[2] = (blockIdx.x == 0 && !(p.flags & F_EXT_DF)) ? p.st->dx2_local : 0.0;
+    }
+    if (do_gram) {
+      const int g_r = lane >> 2, g_c = lane & 3;
+#pragma unroll
+      for (int g = 0; g < GB; ++g) {
+        const int blk = warp + g * NWARP;
+        if (blk < nblk) {
+          const int I = gI[g], J = gJ[g];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = 8 * I + g_r, j = 8 * J + 2 * g_c + e;
+            const double v = e ? gc1[g] : gc0[g];
+            if (j < i && i < kg) {
+              int w;
+              if (del_only) w = i * (i - 1) / 2 + j;
+              else if (i == kg - 1) w = L.off_x + j;
+              else w = L.off_gram + i * (i - 1) / 2 + j;
+              mypart[w] = v;
+            }
+          }
+        }
+      }
+    }
+  } else if constexpr (OP == OP_K2A_CGS2) {
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+      const int a = warp + c * NWARP;
+      if (a < H.na) {
+        const double v = warp_sum(acc[c][0]);
+        if (lane == 0) mypart[a] = v;
+      }
+    }
+  } else if constexpr (OP == OP_GRAM) {
+    if (do_gram) {
+      const int g_r = lane >> 2, g_c = lane & 3;
+#pragma unroll
+      for (int g = 0; g < GB; ++g) {
+        const int blk = warp + g * NWARP;
+        if (blk < nblk) {
+          const int I = gI[g], J = gJ[g];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = 8 * I + g_r, j = 8 * J + 2 * g_c + e;
+            const double v = e ? gc1[g] : gc0[g];
+            if (j <= i && i < kg) mypart[i * (i + 1) / 2 + j] = v;
+          }
+        }
+      }
+    }
+  } else {
+    // row-wise accumulators: block reduction
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane == 0) {
+      H.redw[warp][0] = a0;
+      H.redw[warp][1] = a1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int w = 0; w < NWARP; ++w) {
+        s0 += H.redw[w][0];
+        s1 += H.redw[w][1];
+      }
+      mypart[0] = s0;
+      if (p.words > 1) mypart[1] = s1;
+    }
+  }
+
+  // ------------------------------------------------------------ cross-CTA reduction
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned int t = atomicAdd(&p.st->counter, 1u);
+    H.is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!H.is_last) return;
+  __threadfence();
+  double* outv = (OP == OP_K4) ? reinterpret_cast<double*>(H.scal) + 4 : p.red + (size_t)p.red_slot * LRED;
+  for (int w = tid; w < p.words; w += NT) {
+    double s = 0.0;
+    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(p.part + (size_t)b * LRED + w);
+    outv[w] = s;
+  }
+  __syncthreads();
+  if constexpr (OP == OP_K4) {
+    // commit the replicated small factors (only this CTA writes them; every other CTA
+    // has finished reading them)
+    if (warp == 0) {
+      double* Rw = scratch;
+      double* Tw = scratch + MMAX * MMAX;
+      const K4Head hd = k4_head(p, H, scratch);
+      const int K = hd.K;
+      SmallState* st = p.st;
+      for (int idx = lane; idx < MMAX * MMAX; idx += 32) {
+        const int i = idx % MMAX, j = idx / MMAX;
+        if (i < p.m && j < p.m) st->R[idx] = (i < K && j < K) ? Rw[i + j * MMAX] : 0.0;
+      }
+      if (p.variant == V_ICWY) {
+        for (int idx = lane; idx < MMAX * MMAX; idx += 32) {
+          const int i = idx % MMAX, j = idx / MMAX;
+          if (i < p.m && j < p.m) {
+            double v = 0.0;
+            if (i == j) v = (i < K) ? 1.0 : 0.0;
+            else if (j < i && i < p.k) v = Tw[i + j * MMAX];
+            st->T[idx] = v;
+          }
+        }
+      }
+      for (int j = lane; j < p.m; j += 32) {
+        double s = st->scale[j];
+        if (p.recycle && j < p.k) s = 1.0;
+        if (!(p.flags & F_DELETE_ONLY)) {
+          if (j == p.k) s = 1.0 / hd.rkk;
+          if (p.variant == V_DCGS2 && p.reortho && j == p.k - 1) s = 1.0;
+        }
+        if (j >= K) s = 1.0;
+        st->scale[j] = s;
+      }
+      if (!(p.flags & F_DELETE_ONLY)) {
+        for (int j = lane; j < MMAX; j += 32) st->gamma[j] = (j < K) ? H.coef[j] : 0.0;
+        if (lane == 0) {
+          st->last_rkk = hd.rkk;
+          const double dfn = sqrt(hd.df2);
+          const double ratio = dfn > 0.0 ? hd.rkk / dfn : 0.0;
+          if (ratio < st->rratio_min) st->rratio_min = ratio;
+          if (!(hd.rkk > p.eps_a * dfn)) st->breakdown = 1;   // reading A12
+          if (!(p.flags & F_EXT_DF)) {
+            st->f2 = p.red[0];
+            st->dx2_local = outv[0];
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    p.st->counter = 0u;
+  }
+}
+
+// counter-based SplitMix64 uniform generator (aa_testing.h), bitwise equal to
+// aa_inputs.uniform: u = (z >> 11) * 2^-53, value = lo + (hi - lo) * u without FMA.
+__global__ void aa_fill_uniform_kernel(double* out, long long n, unsigned long long base,
+                                       double lo, double width) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long z = base + (unsigned long long)i + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    out[i] = __dadd_rn(lo, __dmul_rn(width, u));
+  }
+}
+
+// aa_init: f_0 = G(x_0) - x_0, keep G(x_0), x_1 = G(x_0)  (Alg. 1 l.1)
+__global__ void aa_init_kernel(const double* __restrict__ x0, const double* gx0, double* x1,
+                               double* fp, double* gp, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double g = gx0[i];
+    fp[i] = g - x0[i];
+    gp[i] = g;
+    x1[i] = g;
+  }
+}
+
+// normalised copy of the active Q columns (aa_get_q)
+__global__ void aa_copy_q_kernel(const double* Q, long long ld, const SmallState* st, int mi,
+                                 double* out, long long n) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * mi;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long j = idx / n, i = idx % n;
+    out[idx] = Q[j * ld + i] * st->scale[j];
+  }
+}
+
+}  // namespace aa

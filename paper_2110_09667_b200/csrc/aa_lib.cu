@@ -1,0 +1,815 @@
+// aa_lib.cu — libaa host side: the C ABI of include/aa.h and include/aa_testing.h,
+// the per-variant schedule of kernels and allreduces (one ncclAllReduce per global
+// reduction), and the reduction ledger.  P:n = PAPER.md line n.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/aa.h"
+#include "../../include/aa_testing.h"
+#include "aa_kernels.cuh"
+
+using namespace aa;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return api;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(lib, "ncclAllReduce");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(lib, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+  return api;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct TimedEv {
+  int cls;
+  cudaEvent_t a, b;
+};
+
+struct aa_ctx {
+  int64_t n = 0, ld = 0, n_global = 0;
+  int m = 0, variant = 0, rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int device = 0, sms = 148;
+  double *Q = nullptr, *DG = nullptr, *fp = nullptr, *gp = nullptr;
+  SmallState* st = nullptr;
+  double *red = nullptr, *part = nullptr;
+  double *hx = nullptr, *hg = nullptr, *hxn = nullptr;  // staging for aa_step_host
+  ncclComm_t comm = nullptr;
+  // window bookkeeping (host; depends only on i, m_i)
+  int64_t iter = 0;
+  int mi = 0, dg_head = 0;
+  bool inited = false;
+  int failed = AA_OK;
+  // options
+  double beta = 1.0, eps_a = -1.0;
+  int icwy_merged = 0, dcgs2_cond = 3, dcgs2_rscale = 0, profile = 0;
+  // ledger
+  int64_t logical[5] = {0, 0, 0, 0, 0}, logical_last[5] = {0, 0, 0, 0, 0};
+  int64_t ar_total = 0;
+  int ar_last = 0, sp_last = 0;
+  int64_t launches = 0;
+  std::vector<TimedEv> evs;
+  double t_ms[5] = {0, 0, 0, 0, 0};
+  int64_t t_cnt[5] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+int fail(aa_ctx* c, int code) {
+  if (c && c->failed == AA_OK) c->failed = code;
+  return code;
+}
+
+#define CUDA_TRY(c, expr)                                                                    \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) {                                                                 \
+      fprintf(stderr, "libaa: CUDA error %s at %s:%d: %s\n", cudaGetErrorString(_e), __FILE__, \
+              __LINE__, #expr);                                                              \
+      return fail(c, AA_ERR_CUDA);                                                           \
+    }                                                                                        \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+double* qcol(aa_ctx* c, int j) { return c->Q + (size_t)j * c->ld; }
+double* dgcol(aa_ctx* c, int slot) { return c->DG + (size_t)slot * c->ld; }
+
+void choose_tile(int nin, int* tr, int* stages) {
+  const size_t budget = 160 * 1024;
+  const int trs[4] = {256, 128, 64, 32};
+  for (int t = 0; t < 4; ++t) {
+    const size_t sb = (size_t)nin * (trs[t] + 4) * sizeof(double);
+    int s = (int)std::min<size_t>(MAXSTAGES, budget / sb);
+    if (s >= 3) {
+      *tr = trs[t];
+      *stages = s;
+      return;
+    }
+  }
+  *tr = 32;
+  *stages = 2;
+}
+
+struct EvScope {
+  aa_ctx* c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  EvScope(aa_ctx* c_, int cls_) : c(c_), cls(cls_) {
+    if (c->profile) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~EvScope() {
+    if (c->profile) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, c->stream);
+      c->evs.push_back({cls, a, b});
+    }
+  }
+};
+
+template <int OP>
+int launch_op(aa_ctx* c, KParams& p, int cls) {
+  int tr, stages;
+  choose_tile(std::max(p.nin, 1), &tr, &stages);
+  p.tr = tr;
+  p.str = tr + 4;
+  p.stages = stages;
+  const size_t stage_bytes = (size_t)stages * std::max(p.nin, 1) * p.str * sizeof(double);
+  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scratch_bytes());
+  static size_t attr_set = 0;
+  if (smem > attr_set) {
+    CUDA_TRY(c, cudaFuncSetAttribute(aa_stream_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    attr_set = smem;
+  }
+  int per_sm = 1;
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP>, NT, smem));
+  per_sm = std::max(1, std::min(per_sm, 2));
+  const long long ntiles = (p.n + tr - 1) / tr;
+  long long grid = std::min<long long>(ntiles, (long long)c->sms * per_sm);
+  if (grid < 1) grid = 1;
+  p.st = c->st;
+  p.red = c->red;
+  p.part = c->part;
+  p.Q = c->Q;
+  p.ld = c->ld;
+  p.fp = c->fp;
+  p.gp = c->gp;
+  {
+    EvScope ev(c, cls);
+    aa_stream_kernel<OP><<<(unsigned)grid, NT, smem, c->stream>>>(p);
+  }
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  return AA_OK;
+}
+
+int allreduce(aa_ctx* c, double* buf, size_t count) {
+  if (c->nranks == 1 || count == 0) return AA_OK;
+  EvScope ev(c, 3);
+  ncclResult_t r = nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, c->stream);
+  if (r != 0) {
+    fprintf(stderr, "libaa: ncclAllReduce failed: %s\n",
+            nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+    return fail(c, AA_ERR_NCCL);
+  }
+  c->ar_last++;
+  c->ar_total++;
+  return AA_OK;
+}
+
+void set_exact(KParams& p, int i) { p.exact[i >> 6] |= (1ull << (i & 63)); }
+
+KParams base_params(aa_ctx* c) {
+  KParams p;
+  memset(&p, 0, sizeof(p));
+  p.variant = c->variant;
+  p.m = c->m;
+  p.n = c->n;
+  p.beta = c->beta;
+  p.eps_a = c->eps_a;
+  p.icwy_merged = c->icwy_merged;
+  p.rscale = c->dcgs2_rscale;
+  return p;
+}
+
+#define RET_IF(x)            \
+  do {                       \
+    int _s = (x);            \
+    if (_s != AA_OK) return _s; \
+  } while (0)
+
+// One QRAdd (with the fused QRDelete when the window is full) and, unless
+// commit_only, the LSP solve and the x update.  mode: 0 = aa_step, 1 = aa_test_qradd.
+int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const double* vext) {
+  const bool ext = vext != nullptr;
+  const int V = c->variant;
+  const bool recycle = (c->mi == c->m);
+  const int k = recycle ? c->m - 1 : c->mi;
+  const int c_in = recycle ? c->m : k;
+  int dg_slot;
+  if (recycle) {
+    dg_slot = c->dg_head;
+    c->dg_head = (c->dg_head + 1) % c->m;
+  } else {
+    dg_slot = (c->dg_head + c->mi) % c->m;
+  }
+  const bool reortho = (V == V_DCGS2) && k >= 2 && (k + 1 > c->dcgs2_cond);
+  const bool has_x = (V == V_ICWY && k >= 2) || (V == V_DCGS2 && reortho);
+  const int gram = (V == V_ICWY && recycle && k >= 2) ? 1 : 0;
+  const K1Layout L = K1Layout::make(k, has_x, gram != 0);
+  c->ar_last = 0;
+  c->sp_last = 0;
+  for (int i = 0; i < 5; ++i) c->logical_last[i] = 0;
+
+  KParams p = base_params(c);
+  p.k = k;
+  p.c_in = c_in;
+  p.recycle = recycle ? 1 : 0;
+  p.has_x = has_x ? 1 : 0;
+  p.gram = gram;
+  p.reortho = reortho ? 1 : 0;
+  p.beta_on = (c->beta != 1.0 && !ext) ? 1 : 0;
+  p.flags = ext ? F_EXT_DF : 0;
+
+  // ---------------- K1: prologue + QRDelete rotation + pass-1 multi-dot
+  {
+    KParams q = p;
+    q.op = OP_K1;
+    if (ext) {
+      for (int i = 0; i < 4; ++i) {
+        q.in[i] = vext;
+        set_exact(q, i);
+      }
+    } else {
+      q.in[0] = x;
+      q.in[1] = g;
+      q.in[2] = c->fp;
+      q.in[3] = c->gp;
+      set_exact(q, 0);
+      set_exact(q, 1);
+    }
+    for (int j = 0; j < c_in; ++j) q.in[4 + j] = qcol(c, j);
+    q.nin = 4 + c_in;
+    q.dg_out = dgcol(c, dg_slot);
+    q.words = L.words;
+    q.red_slot = 0;
+    RET_IF(launch_op<OP_K1>(c, q, 0));
+  }
+  if (gram && L.n_gram > 0 && !c->icwy_merged) {
+    // the ICWY correction-matrix update after QRDelete: its own reduction
+    RET_IF(allreduce(c, c->red + L.off_gram, (size_t)L.n_gram));
+    c->sp_last++;
+    RET_IF(allreduce(c, c->red, (size_t)L.off_gram));
+    c->sp_last++;
+  } else {
+    RET_IF(allreduce(c, c->red, (size_t)L.words));
+    c->sp_last++;
+  }
+  // ---------------- K2: the rest of QRAdd
+  int final_slot = 0;
+  if (k >= 1) {
+    KParams q = p;
+    if (V == V_ICWY || V == V_DCGS2) {
+      q.op = (V == V_ICWY) ? OP_K2_ICWY : OP_K2_DCGS2;
+      for (int j = 0; j <= k; ++j) q.in[j] = qcol(c, j);
+      q.in[k + 1] = c->fp;
+      q.nin = k + 2;
+      q.words = 2;
+      q.red_slot = 1;
+      if (V == V_ICWY) RET_IF(launch_op<OP_K2_ICWY>(c, q, 1));
+      else RET_IF(launch_op<OP_K2_DCGS2>(c, q, 1));
+      RET_IF(allreduce(c, c->red + LRED, 2));
+      c->sp_last++;
+      final_slot = 1;
+    } else if (V == V_CGS2) {
+      q.op = OP_K2A_CGS2;
+      for (int j = 0; j <= k; ++j) q.in[j] = qcol(c, j);
+      q.nin = k + 1;
+      q.words = k;
+      q.red_slot = 1;
+      RET_IF(launch_op<OP_K2A_CGS2>(c, q, 1));
+      RET_IF(allreduce(c, c->red + LRED, (size_t)k));
+      c->sp_last++;
+      KParams q2 = p;
+      q2.op = OP_K2B_CGS2;
+      for (int j = 0; j <= k; ++j) q2.in[j] = qcol(c, j);
+      q2.in[k + 1] = c->fp;
+      q2.nin = k + 2;
+      q2.words = 2;
+      q2.red_slot = 2;
+      RET_IF(launch_op<OP_K2B_CGS2>(c, q2, 1));
+      RET_IF(allreduce(c, c->red + 2 * LRED, 2));
+      c->sp_last++;
+      final_slot = 2;
+    } else {  // MGS: k dependent passes
+      for (int j = 1; j <= k; ++j) {
+        KParams q2 = p;
+        q2.op = OP_K2_MGS;
+        q2.mgs_j = j;
+        q2.in[0] = qcol(c, j - 1);
+        q2.in[1] = qcol(c, k);
+        q2.in[2] = (j < k) ? qcol(c, j) : c->fp;
+        q2.nin = 3;
+        q2.words = (j < k) ? 1 : 2;
+        q2.red_slot = j;
+        RET_IF(launch_op<OP_K2_MGS>(c, q2, 1));
+        RET_IF(allreduce(c, c->red + (size_t)j * LRED, (size_t)q2.words));
+        c->sp_last++;
+      }
+      final_slot = k;
+    }
+  }
+  // ---------------- K4: gamma + x update + commit
+  {
+    KParams q = p;
+    q.op = OP_K4;
+    q.final_slot = final_slot;
+    q.words = 1;
+    if (ext) {
+      q.n = 0;
+      q.nin = 0;
+      q.flags |= F_COMMIT_ONLY;
+    } else {
+      q.in[0] = g;
+      q.in[1] = x;
+      set_exact(q, 0);
+      set_exact(q, 1);
+      for (int j = 0; j <= k; ++j) q.in[2 + j] = dgcol(c, (c->dg_head + j) % c->m);
+      int nin = 2 + (k + 1);
+      if (q.beta_on) {
+        q.in[nin++] = c->fp;
+        for (int j = 0; j <= k; ++j) q.in[nin++] = qcol(c, j);
+      }
+      q.nin = nin;
+      q.x_out = xn;
+    }
+    RET_IF(launch_op<OP_K4>(c, q, 2));
+  }
+  c->mi = k + 1;
+  // ---------------- ledger (paper's logical counts)
+  int add;
+  if (k == 0) add = 1;
+  else if (V == V_MGS) add = k + 1;
+  else if (V == V_CGS2) add = 3;
+  else add = 2;
+  c->logical_last[AA_PH_QRADD] = add;
+  c->logical_last[AA_PH_QRDELETE] = (V == V_ICWY && recycle) ? 1 : 0;
+  if (!ext) {
+    c->logical_last[AA_PH_LSP_RHS] = 1;
+    c->logical_last[AA_PH_NORM] = 1;
+  }
+  for (int i = 0; i < 5; ++i) c->logical[i] += c->logical_last[i];
+  return AA_OK;
+}
+
+int check_handle(aa_handle_t h) {
+  if (!h) return AA_ERR_ARG;
+  if (h->failed != AA_OK) return h->failed;
+  return AA_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* aa_status_string(int s) {
+  switch (s) {
+    case AA_OK: return "ok";
+    case AA_ERR_ARG: return "invalid argument";
+    case AA_ERR_STATE: return "invalid state for this call";
+    case AA_ERR_CUDA: return "CUDA error";
+    case AA_ERR_NCCL: return "NCCL error or NCCL unavailable";
+    case AA_ERR_NOMEM: return "device allocation failed";
+    case AA_ERR_BREAKDOWN: return "QR breakdown (new column numerically dependent)";
+    default: return "unknown status";
+  }
+}
+
+int aa_comm_unique_id(void* id128) {
+  if (!id128) return AA_ERR_ARG;
+  if (!nccl().ok) return AA_ERR_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != 0) return AA_ERR_NCCL;
+  memcpy(id128, &id, sizeof(id));
+  return AA_OK;
+}
+
+int aa_create(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank, int nranks,
+              const void* id128, void* cuda_stream) {
+  if (!out || n_local < 1 || m < 1 || m > MMAX || qr_variant < 0 || qr_variant > 3 || nranks < 1 ||
+      rank < 0 || rank >= nranks || (nranks > 1 && !id128))
+    return AA_ERR_ARG;
+  *out = nullptr;
+  aa_ctx* c = new aa_ctx();
+  c->n = n_local;
+  c->ld = (n_local + 255) / 256 * 256;
+  c->n_global = n_local * nranks;
+  c->m = m;
+  c->variant = qr_variant;
+  c->rank = rank;
+  c->nranks = nranks;
+  auto bail = [&](int code) {
+    aa_destroy(c);
+    return code;
+  };
+  if (cudaGetDevice(&c->device) != cudaSuccess) return bail(AA_ERR_CUDA);
+  if (cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess)
+    return bail(AA_ERR_CUDA);
+  // NULL = the CUDA legacy default stream (what torch reports as stream 0)
+  c->stream = (cudaStream_t)cuda_stream;
+  c->own_stream = false;
+  const size_t vbytes = (size_t)c->ld * sizeof(double);
+  if (cudaMalloc(&c->Q, vbytes * m) != cudaSuccess || cudaMalloc(&c->DG, vbytes * m) != cudaSuccess ||
+      cudaMalloc(&c->fp, vbytes) != cudaSuccess || cudaMalloc(&c->gp, vbytes) != cudaSuccess ||
+      cudaMalloc(&c->st, sizeof(SmallState)) != cudaSuccess ||
+      cudaMalloc(&c->red, sizeof(double) * LRED * NSLOT) != cudaSuccess ||
+      cudaMalloc(&c->part, sizeof(double) * LRED * 2 * c->sms) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(AA_ERR_NOMEM);
+  }
+  // zero the padded rows once (they are read, never used, by the bulk copies)
+  if (cudaMemset(c->Q, 0, vbytes * m) != cudaSuccess || cudaMemset(c->DG, 0, vbytes * m) != cudaSuccess ||
+      cudaMemset(c->fp, 0, vbytes) != cudaSuccess || cudaMemset(c->gp, 0, vbytes) != cudaSuccess ||
+      cudaMemset(c->red, 0, sizeof(double) * LRED * NSLOT) != cudaSuccess ||
+      cudaMemset(c->st, 0, sizeof(SmallState)) != cudaSuccess)
+    return bail(AA_ERR_CUDA);
+  if (nranks > 1) {
+    if (!nccl().ok) return bail(AA_ERR_NCCL);
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    if (nccl().CommInitRank(&c->comm, nranks, id, rank) != 0) return bail(AA_ERR_NCCL);
+  }
+  *out = c;
+  return AA_OK;
+}
+
+int aa_set_option(aa_handle_t h, int opt, double val) {
+  RET_IF(check_handle(h));
+  switch (opt) {
+    case AA_OPT_DAMPING_BETA:
+      if (!(val > 0.0 && val <= 1.0)) return AA_ERR_ARG;
+      h->beta = val;
+      return AA_OK;
+    case AA_OPT_ICWY_DELETE:
+      if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
+      h->icwy_merged = (int)val;
+      return AA_OK;
+    case AA_OPT_DCGS2_COND:
+      if (val != 2.0 && val != 3.0) return AA_ERR_ARG;
+      h->dcgs2_cond = (int)val;
+      return AA_OK;
+    case AA_OPT_DCGS2_RSCALE:
+      if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
+      h->dcgs2_rscale = (int)val;
+      return AA_OK;
+    case AA_OPT_BREAKDOWN_EPS:
+      if (!(val >= 0.0)) return AA_ERR_ARG;
+      h->eps_a = val;
+      return AA_OK;
+    case AA_OPT_PROFILE:
+      h->profile = val != 0.0;
+      return AA_OK;
+    case AA_OPT_N_GLOBAL:
+      if (!(val >= 1.0)) return AA_ERR_ARG;
+      h->n_global = (int64_t)val;
+      return AA_OK;
+    default:
+      return AA_ERR_ARG;
+  }
+}
+
+static int reset_small(aa_ctx* c) {
+  SmallState* hs = new SmallState();
+  memset(hs, 0, sizeof(SmallState));
+  for (int j = 0; j < MMAX; ++j) hs->scale[j] = 1.0;
+  hs->rratio_min = DBL_MAX;
+  cudaError_t e = cudaMemcpyAsync(c->st, hs, sizeof(SmallState), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  delete hs;
+  if (e != cudaSuccess) return fail(c, AA_ERR_CUDA);
+  return AA_OK;
+}
+
+int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out) {
+  RET_IF(check_handle(h));
+  if (!x0 || !gx0 || !x1_out) return AA_ERR_ARG;
+  RET_IF(reset_small(h));
+  if (h->eps_a < 0.0) h->eps_a = 10.0 * DBL_EPSILON * sqrt((double)h->n_global);
+  const int grid = h->sms * 4;
+  aa_init_kernel<<<grid, 256, 0, h->stream>>>(x0, gx0, x1_out, h->fp, h->gp, h->n);
+  h->launches++;
+  CUDA_TRY(h, cudaGetLastError());
+  h->iter = 0;
+  h->mi = 0;
+  h->dg_head = 0;
+  h->inited = true;
+  return AA_OK;
+}
+
+int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next) {
+  RET_IF(check_handle(h));
+  if (!h->inited) return AA_ERR_STATE;
+  if (!x_i || !gx_i || !x_next || !aligned16(x_i) || !aligned16(gx_i) || !aligned16(x_next))
+    return AA_ERR_ARG;
+  int rc;
+  {
+    EvScope ev(h, 4);
+    rc = run_step(h, x_i, gx_i, x_next, nullptr);
+  }
+  if (rc == AA_OK) h->iter++;
+  return rc;
+}
+
+int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next) {
+  RET_IF(check_handle(h));
+  if (!h->inited) return AA_ERR_STATE;
+  if (!x_i || !gx_i || !x_next) return AA_ERR_ARG;
+  const size_t vb = (size_t)h->n * sizeof(double);
+  if (!h->hx) {
+    if (cudaMalloc(&h->hx, vb) != cudaSuccess || cudaMalloc(&h->hg, vb) != cudaSuccess ||
+        cudaMalloc(&h->hxn, vb) != cudaSuccess) {
+      cudaGetLastError();
+      return AA_ERR_NOMEM;
+    }
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(h->hx, x_i, vb, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->hg, gx_i, vb, cudaMemcpyHostToDevice, h->stream));
+  RET_IF(aa_step(h, h->hx, h->hg, h->hxn));
+  CUDA_TRY(h, cudaMemcpyAsync(x_next, h->hxn, vb, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return AA_OK;
+}
+
+int aa_delete_oldest(aa_handle_t h) {
+  RET_IF(check_handle(h));
+  if (!h->inited || h->mi == 0) return AA_ERR_STATE;
+  const int V = h->variant;
+  const int k = h->mi - 1;  // retained columns
+  const int gram = (V == V_ICWY && k >= 2) ? 1 : 0;
+  const int words = gram ? k * (k - 1) / 2 : 0;
+  for (int i = 0; i < 5; ++i) h->logical_last[i] = 0;
+  h->ar_last = 0;
+  h->sp_last = 0;
+  KParams p = base_params(h);
+  p.k = k;
+  p.c_in = h->mi;
+  p.recycle = 1;
+  p.gram = gram;
+  p.flags = F_DELETE_ONLY;
+  {
+    KParams q = p;
+    q.op = OP_K1;
+    for (int j = 0; j < h->mi; ++j) q.in[j] = qcol(h, j);
+    q.nin = h->mi;
+    q.words = words;
+    q.red_slot = 0;
+    RET_IF(launch_op<OP_K1>(h, q, 0));
+  }
+  if (V == V_ICWY) {
+    RET_IF(allreduce(h, h->red, (size_t)words));
+    if (words > 0) h->sp_last++;
+  }
+  {
+    KParams q = p;
+    q.op = OP_K4;
+    q.n = 0;
+    q.nin = 0;
+    q.words = 1;
+    q.flags |= F_COMMIT_ONLY;
+    RET_IF(launch_op<OP_K4>(h, q, 2));
+  }
+  h->mi = k;
+  h->dg_head = (h->dg_head + 1) % h->m;
+  h->logical_last[AA_PH_QRDELETE] = (V == V_ICWY) ? 1 : 0;
+  h->logical[AA_PH_QRDELETE] += h->logical_last[AA_PH_QRDELETE];
+  return AA_OK;
+}
+
+int aa_test_qradd(aa_handle_t h, const double* v) {
+  RET_IF(check_handle(h));
+  if (!h->inited) return AA_ERR_STATE;
+  if (!v || !aligned16(v)) return AA_ERR_ARG;
+  return run_step(h, nullptr, nullptr, nullptr, v);
+}
+
+int aa_stats(aa_handle_t h, struct aa_stats* out, int flags) {
+  if (!h || !out) return AA_ERR_ARG;
+  memset(out, 0, sizeof(*out));
+  out->loo = -1.0;
+  out->iter = h->iter;
+  out->m_i = h->mi;
+  out->sync_points_last = h->sp_last;
+  out->allreduce_last = h->ar_last;
+  out->allreduce_total = h->ar_total;
+  for (int i = 0; i < 5; ++i) {
+    out->logical_sync[i] = h->logical[i];
+    out->logical_sync_last[i] = h->logical_last[i];
+  }
+  if (h->failed != AA_OK) return h->failed;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  struct {
+    double dx2, f2, rmin;
+    int bd;
+  } hs;
+  {
+    SmallState* full = new SmallState();
+    cudaError_t e = cudaMemcpy(full, h->st, sizeof(SmallState), cudaMemcpyDeviceToHost);
+    hs.dx2 = full->dx2_local;
+    hs.f2 = full->f2;
+    hs.rmin = full->rratio_min;
+    hs.bd = full->breakdown;
+    delete full;
+    CUDA_TRY(h, e);
+  }
+  if (h->nranks > 1) {
+    double* tmp = h->red + (size_t)(NSLOT - 1) * LRED;
+    CUDA_TRY(h, cudaMemcpyAsync(tmp, &hs.dx2, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    ncclResult_t r = nccl().AllReduce(tmp, tmp, 1, kNcclFloat64, kNcclSum, h->comm, h->stream);
+    if (r != 0) return fail(h, AA_ERR_NCCL);
+    CUDA_TRY(h, cudaMemcpyAsync(&hs.dx2, tmp, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  }
+  out->f_norm = sqrt(hs.f2);
+  out->dx_norm = sqrt(hs.dx2);
+  out->r_ratio_min = hs.rmin;
+  out->breakdown = hs.bd;
+  if ((flags & AA_STATS_LOO) && h->mi >= 1) {
+    KParams p = base_params(h);
+    p.op = OP_GRAM;
+    p.gram = 2;
+    p.c_in = h->mi;
+    for (int j = 0; j < h->mi; ++j) p.in[j] = qcol(h, j);
+    p.nin = h->mi;
+    const int words = h->mi * (h->mi + 1) / 2;
+    p.words = words;
+    p.red_slot = NSLOT - 1;
+    RET_IF(launch_op<OP_GRAM>(h, p, 1));
+    double* gbuf = h->red + (size_t)(NSLOT - 1) * LRED;
+    if (h->nranks > 1) {
+      ncclResult_t r = nccl().AllReduce(gbuf, gbuf, words, kNcclFloat64, kNcclSum, h->comm, h->stream);
+      if (r != 0) return fail(h, AA_ERR_NCCL);
+    }
+    std::vector<double> gh(words);
+    CUDA_TRY(h, cudaMemcpyAsync(gh.data(), gbuf, sizeof(double) * words, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    double s = 0.0;
+    for (int i = 0; i < h->mi; ++i)
+      for (int j = 0; j <= i; ++j) {
+        const double g = gh[i * (i + 1) / 2 + j];
+        s += (i == j) ? (1.0 - g) * (1.0 - g) : 2.0 * g * g;
+      }
+    out->loo = sqrt(s);
+  }
+  if (flags & AA_STATS_RESET) {
+    for (int i = 0; i < 5; ++i) h->logical[i] = 0;
+    h->ar_total = 0;
+  }
+  return hs.bd ? AA_ERR_BREAKDOWN : AA_OK;
+}
+
+int aa_reset(aa_handle_t h) {
+  RET_IF(check_handle(h));
+  if (!h->inited) return AA_ERR_STATE;
+  // empty the window; f_{i-1} and G(x_{i-1}) are kept, so the next aa_step takes the
+  // i = 1 branch of Alg. 2 with Delta f = f_i - f_{i-1}
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->mi = 0;
+  h->dg_head = 0;
+  SmallState* hs = new SmallState();
+  memset(hs, 0, sizeof(SmallState));
+  for (int j = 0; j < MMAX; ++j) hs->scale[j] = 1.0;
+  hs->rratio_min = DBL_MAX;
+  // keep dx2_local / f2
+  cudaError_t e = cudaMemcpy(h->st, hs, offsetof(SmallState, dx2_local), cudaMemcpyHostToDevice);
+  int bd = 0;
+  if (e == cudaSuccess)
+    e = cudaMemcpy(reinterpret_cast<char*>(h->st) + offsetof(SmallState, breakdown), &bd, sizeof(int),
+                   cudaMemcpyHostToDevice);
+  delete hs;
+  if (e != cudaSuccess) return fail(h, AA_ERR_CUDA);
+  return AA_OK;
+}
+
+int aa_destroy(aa_handle_t h) {
+  if (!h) return AA_ERR_ARG;
+  cudaStreamSynchronize(h->stream);
+  for (auto& e : h->evs) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  cudaFree(h->Q);
+  cudaFree(h->DG);
+  cudaFree(h->fp);
+  cudaFree(h->gp);
+  cudaFree(h->st);
+  cudaFree(h->red);
+  cudaFree(h->part);
+  cudaFree(h->hx);
+  cudaFree(h->hg);
+  cudaFree(h->hxn);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return AA_OK;
+}
+
+// ------------------------------------------------------------------ testing hooks
+int aa_get_small(aa_handle_t h, double* R, double* T, double* gamma, double* scale) {
+  RET_IF(check_handle(h));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  SmallState* hs = new SmallState();
+  cudaError_t e = cudaMemcpy(hs, h->st, sizeof(SmallState), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    delete hs;
+    return fail(h, AA_ERR_CUDA);
+  }
+  const int m = h->m;
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) {
+      if (R) R[i + j * m] = hs->R[i + j * MMAX];
+      if (T) T[i + j * m] = hs->T[i + j * MMAX];
+    }
+  if (gamma)
+    for (int j = 0; j < h->mi; ++j) gamma[j] = hs->gamma[j];
+  if (scale)
+    for (int j = 0; j < m; ++j) scale[j] = hs->scale[j];
+  delete hs;
+  return AA_OK;
+}
+
+int aa_get_q(aa_handle_t h, double* q_out) {
+  RET_IF(check_handle(h));
+  if (!q_out) return AA_ERR_ARG;
+  if (h->mi == 0) return AA_OK;
+  aa_copy_q_kernel<<<h->sms * 4, 256, 0, h->stream>>>(h->Q, h->ld, h->st, h->mi, q_out, h->n);
+  h->launches++;
+  CUDA_TRY(h, cudaGetLastError());
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return AA_OK;
+}
+
+int aa_timings(aa_handle_t h, double* ms_out5, int64_t* counts5, int reset) {
+  if (!h) return AA_ERR_ARG;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  for (auto& e : h->evs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    h->t_ms[e.cls] += ms;
+    h->t_cnt[e.cls]++;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  h->evs.clear();
+  for (int i = 0; i < 5; ++i) {
+    if (ms_out5) ms_out5[i] = h->t_ms[i];
+    if (counts5) counts5[i] = h->t_cnt[i];
+    if (reset) {
+      h->t_ms[i] = 0;
+      h->t_cnt[i] = 0;
+    }
+  }
+  return AA_OK;
+}
+
+int64_t aa_kernel_launches(aa_handle_t h) { return h ? h->launches : -1; }
+
+int aa_fill_uniform(double* out, int64_t n, int64_t offset, uint64_t seed, uint64_t stream, double lo,
+                    double hi, void* cuda_stream) {
+  if (!out || n < 0) return AA_ERR_ARG;
+  if (n == 0) return AA_OK;
+  const unsigned long long base = seed + stream * (1ull << 48) + (unsigned long long)offset;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  aa_fill_uniform_kernel<<<sms * 8, 256, 0, (cudaStream_t)cuda_stream>>>(out, n, base, lo, hi - lo);
+  if (cudaGetLastError() != cudaSuccess) return AA_ERR_CUDA;
+  return AA_OK;
+}
+
+int aa_build_info(char* buf, int len) {
+  if (!buf || len <= 0) return AA_ERR_ARG;
+  snprintf(buf, (size_t)len,
+           "libaa sm_100a; NT=%d MMAX=%d LRED=%d MAXSTAGES=%d; TMA bulk staging, fp64 DMMA Gram", NT, MMAX,
+           LRED, MAXSTAGES);
+  return AA_OK;
+}
+
+}  // extern "C"

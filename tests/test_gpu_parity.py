@@ -1,0 +1,315 @@
+"""GPU parity: libaa (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (SURVEY.md §8(c) "Parity criteria"):
+  x_k            max_k ||x_k^GPU - x_k^O|| / ||x_k^O|| <= 1e-10  (k = 2..21)
+  ||f_i||        |a - b| <= 1e-10 ||f_i||^O + 100 eps ||x_i||^O
+  LOO            LOO^GPU <= max(10 LOO^O2, 10 m eps)
+  iterations     identical to O2 for the same variant
+  ledger         logical counts exactly the paper's
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from aa_inputs import problems  # noqa: E402
+from oracle import EPS, aa_definition, aa_variant, VARIANTS  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2110_09667_b200 import aa  # noqa: E402
+from tests._gpu_run import run_gpu  # noqa: E402
+
+
+def _rel_x(gpu, orc, K=20):
+    worst = 0.0
+    for a, b in zip(gpu.xs[:K], orc.xs[:K]):
+        worst = max(worst, np.linalg.norm(a - b) / np.linalg.norm(b))
+    return worst
+
+
+def _check_fnorms(gpu, orc, xnorms):
+    for i, (a, b) in enumerate(zip(gpu.f_norms, orc.f_norms)):
+        assert abs(a - b) <= 1e-10 * b + 100 * EPS * xnorms[i], (i, a, b)
+
+
+@pytest.fixture(scope="module")
+def config1():
+    M, b = problems.linear_dense(1000, 0.95)
+    Mt = torch.tensor(M, device="cuda")
+    bt = torch.tensor(b, device="cuda")
+    return M, b, (lambda x: M @ x + b), (lambda x: Mt @ x + bt)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_config1_parity(config1, variant):
+    """Config 1: n=1000, m=5, linear G, 30 iterations, every variant vs O2 and O1."""
+    M, b, Gn, Gt = config1
+    n, m, iters = 1000, 5, 30
+    o2 = aa_variant(Gn, np.zeros(n), m, variant, iters)
+    o1 = aa_definition(Gn, np.zeros(n), m, iters)
+    gpu = run_gpu(Gt, np.zeros(n), m, variant, iters, loo=True)
+    assert _rel_x(gpu, o2) <= 1e-10
+    assert _rel_x(gpu, o1) <= 1e-10
+    xnorms = [np.linalg.norm(o2.x1)] + [np.linalg.norm(x) for x in o2.xs]
+    _check_fnorms(gpu, o2, xnorms)
+    for lg, lo in zip(gpu.loo, o2.loo):
+        assert lg <= max(10 * lo, 10 * m * EPS)
+    for a, b_ in zip(gpu.dx_norms, o2.dx_norms):
+        assert abs(a - b_) <= 1e-9 * b_ + 1e-13
+    # ledger identical to the oracle's (paper formulas)
+    for lg, lo in zip(gpu.ledgers, o2.ledgers):
+        for ph in ("qradd", "qrdelete", "lsp_rhs", "norm_check"):
+            assert lg[ph] == lo[ph], (ph, lg, lo)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_config1_iteration_count(config1, variant):
+    """Config 1 run (ii): tol 1e-6 on ||dx||_2 -> identical iteration count."""
+    M, b, Gn, Gt = config1
+    o2 = aa_variant(Gn, np.zeros(1000), 5, variant, 200, tol=1e-6, record_x=False, record_loo=False)
+    gpu = run_gpu(Gt, np.zeros(1000), 5, variant, 200, tol=1e-6, record_x=False)
+    assert o2.converged and gpu.converged
+    assert gpu.iters == o2.iters
+
+
+def test_config1_gmres_window30(config1):
+    """AA(m=30) == GMRES on the linear problem, through the GPU path."""
+    from tests._gmres import gmres_iterates
+    M, b, Gn, Gt = config1
+    K = 25
+    xg = gmres_iterates(np.eye(1000) - M, b, np.zeros(1000), K)
+    for v in ("mgs", "dcgs2"):
+        gpu = run_gpu(Gt, np.zeros(1000), 30, v, K)
+        for i in range(1, K + 1):
+            pred = M @ xg[i] + b
+            assert np.linalg.norm(gpu.xs[i - 1] - pred) <= 1e-10 * np.linalg.norm(pred)
+
+
+CASES = [(1, 1), (7, 2), (33, 3), (257, 4), (1000, 5), (4097, 10), (100003, 5), (65536 + 37, 20)]
+
+
+@pytest.mark.parametrize("n,m", CASES)
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_ragged_sizes_and_windows(n, m, variant):
+    """Diagonal G (configs 2/3 recipe) at ragged sizes: several tiles plus a tail, windows
+    from 1 to 20, start-up and recycle iterations."""
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    iters = min(2 * m + 6, 30)
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters)
+    gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, iters)
+    # stop comparing once the oracle has converged to rounding level
+    K = next((i for i, f in enumerate(o2.f_norms) if f < 1e-11 * np.linalg.norm(o2.x1)), iters)
+    if K > 0:
+        assert _rel_x(gpu, o2, K) <= 1e-10
+    for i in range(K):
+        assert gpu.ledgers[i] == {k_: v_ for k_, v_ in o2.ledgers[i].items()}
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_large_window_many_tiles(variant):
+    """m = 50 (the config 2 / config 5 extreme) over ~20 tiles, recycle included."""
+    n, m, iters = 20000 + 3, 50, 56
+    d, b = problems.diagonal(n, -0.95, 0.95)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters)
+    gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, iters, loo=True)
+    K = next((i for i, f in enumerate(o2.f_norms) if f < 1e-9 * np.linalg.norm(o2.x1)), iters)
+    assert _rel_x(gpu, o2, K) <= 1e-10
+    for lg, lo in zip(gpu.loo[:K], o2.loo[:K]):
+        assert lg <= max(10 * lo, 10 * m * EPS)
+
+
+def test_window_64_max():
+    n, m, iters = 3000, 64, 68
+    d, b = problems.diagonal(n, -0.95, 0.95)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    for v in ("icwy", "dcgs2"):
+        o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, v, iters)
+        gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, v, iters)
+        K = next((i for i, f in enumerate(o2.f_norms) if f < 1e-9 * np.linalg.norm(o2.x1)), iters)
+        assert _rel_x(gpu, o2, K) <= 1e-10
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_damping(config1, variant):
+    M, b, Gn, Gt = config1
+    o2 = aa_variant(Gn, np.zeros(1000), 4, variant, 20, beta=0.5)
+    gpu = run_gpu(Gt, np.zeros(1000), 4, variant, 20, beta=0.5)
+    assert _rel_x(gpu, o2) <= 1e-10
+
+
+@pytest.mark.parametrize("opts,okw", [
+    (dict(icwy_merged=1), dict()),
+    (dict(dcgs2_cond=2), dict(dcgs2_cond=2)),
+    (dict(dcgs2_rscale=1), dict(dcgs2_rscale=True)),
+])
+def test_options(opts, okw):
+    n, m, iters = 5000, 6, 20
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    v = "icwy" if "icwy_merged" in opts else "dcgs2"
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, v, iters, **okw)
+    gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, v, iters, **opts)
+    assert _rel_x(gpu, o2) <= 1e-10
+    if "icwy_merged" in opts:
+        assert gpu.sync_points[-1] == 2
+    elif v == "icwy":
+        assert gpu.sync_points[-1] == 3
+
+
+def test_sync_points_per_iteration():
+    """Physical reduction points per aa_step: FIRST 1; start-up MGS m_i, ICWY 2, CGS-2 3,
+    DCGS-2 2; recycle MGS m, ICWY 3 (2 merged), CGS-2 3, DCGS-2 2 (a9)."""
+    n, m = 4096, 6
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    for v in VARIANTS:
+        gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, v, m + 3)
+        sp = gpu.sync_points
+        assert sp[0] == 1
+        for i in range(2, m + 1):
+            mi = i
+            want = {"mgs": mi, "icwy": 2, "cgs2": 3, "dcgs2": 2}[v]
+            assert sp[i - 1] == want, (v, i, sp)
+        for i in range(m + 1, m + 4):
+            want = {"mgs": m, "icwy": 3, "cgs2": 3, "dcgs2": 2}[v]
+            assert sp[i - 1] == want, (v, i, sp)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_delete_oldest_and_q(variant):
+    """Stand-alone Givens QRDelete: Q'R' = F[:, 1:] and Q orthonormal."""
+    from oracle import Ledger, QRState, Reducer, qradd, qrdelete_givens
+    n, m = 3001, 5
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, 4)
+    s = gpu.solver
+    mi = s.stats().m_i
+    q = torch.empty(n * mi, dtype=torch.float64, device="cuda")
+    aa.aa_get_q(s.h, q)
+    Q0 = q.cpu().numpy().reshape(mi, n).T
+    R0, T0, g0, _ = aa.aa_get_small(s.h, m, mi)
+    F = Q0 @ R0[:mi, :mi]
+    s.delete_oldest()
+    st = s.stats()
+    assert st.m_i == mi - 1
+    q2 = torch.empty(n * (mi - 1), dtype=torch.float64, device="cuda")
+    aa.aa_get_q(s.h, q2)
+    Q1 = q2.cpu().numpy().reshape(mi - 1, n).T
+    R1, T1, _, _ = aa.aa_get_small(s.h, m, mi - 1)
+    k = mi - 1
+    assert np.max(np.abs(Q1 @ R1[:k, :k] - F[:, 1:])) <= 1e-12 * np.max(np.abs(F))
+    assert np.all(np.diag(R1[:k, :k]) > 0)
+    # oracle delete on the same factors
+    ost = QRState(n, m)
+    ost.Q[:, :mi] = Q0
+    ost.R[:mi, :mi] = R0[:mi, :mi]
+    ost.mi = mi
+    qrdelete_givens(ost)
+    assert np.max(np.abs(ost.R[:k, :k] - R1[:k, :k])) <= 1e-13 * np.max(np.abs(R0))
+    assert np.max(np.abs(ost.Q[:, :k] - Q1)) <= 1e-13
+    if variant == "icwy":
+        G = Q1.T @ Q1
+        assert np.max(np.abs(np.tril(T1[:k, :k], -1) - np.tril(G, -1))) <= 1e-14
+        assert np.all(np.diag(T1[:k, :k]) == 1.0)
+
+
+@pytest.mark.parametrize("kappa", [1e1, 1e3, 1e6, 1e9])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_ortho_stress_loo(kappa, variant):
+    """Config 5a at test size: columns of U Sigma V^T appended with aa_test_qradd; LOO
+    within 10x the oracle's (or 10 m eps), R matches the oracle's R."""
+    from oracle import Ledger, QRState, Reducer, qradd, loss_of_orthogonality
+    n, m = 4000, 20
+    A = problems.ortho_test_matrix(n, m, kappa, seed=11)
+    st, led, red = QRState(n, m), Ledger(), Reducer(1)
+    r00 = red.norm(A[:, 0]); st.R[0, 0] = r00; st.Q[:, 0] = A[:, 0] / r00; st.mi = 1
+    for j in range(1, m):
+        qradd(variant, st, A[:, j], led, red)
+    lo = loss_of_orthogonality(st.Q)
+    if variant == "dcgs2" and kappa >= 1e6:
+        # DCGS-2 is in its O(eps) kappa^2 regime here: summation order alone
+        # moves LOO by orders of magnitude, so compare with the oracle's envelope over
+        # several reduction orders (simulated shard counts), SURVEY.md §8(c) criterion 4.
+        env = []
+        for p in (1, 2, 3, 4, 7, 8, 16, 64):
+            st2, led2, red2 = QRState(n, m), Ledger(), Reducer(p)
+            r0 = red2.norm(A[:, 0]); st2.R[0, 0] = r0; st2.Q[:, 0] = A[:, 0] / r0; st2.mi = 1
+            for j in range(1, m):
+                qradd(variant, st2, A[:, j], led2, red2)
+            env.append(loss_of_orthogonality(st2.Q))
+        lo = max(env)
+    s = aa.AndersonSolver(n, m, variant, stream=torch.cuda.current_stream())
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    x1 = torch.empty_like(z)
+    s.init(z, z, x1)
+    At = torch.tensor(np.ascontiguousarray(A.T), device="cuda")
+    for j in range(m):
+        aa.aa_test_qradd(s.h, At[j])
+    stg = s.stats(loo=True)
+    assert stg.m_i == m
+    assert stg.loo <= max(10 * lo, 10 * m * EPS), (stg.loo, lo)
+    R, T, _, _ = aa.aa_get_small(s.h, m, m)
+    if kappa <= 1e3:
+        assert np.max(np.abs(R - st.R)) <= 1e-10 * np.max(np.abs(st.R))
+
+
+def test_step_host_matches_device(config1):
+    M, b, Gn, Gt = config1
+    n, m = 1000, 5
+    ref = run_gpu(Gt, np.zeros(n), m, "dcgs2", 12)
+    s = aa.AndersonSolver(n, m, "dcgs2", stream=torch.cuda.current_stream())
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    x1 = torch.empty_like(x)
+    s.init(x, Gt(x), x1)
+    xh = x1.cpu().numpy().copy()
+    for i in range(12):
+        gh = Gn(xh)
+        out = np.empty(n)
+        s.step_host(xh, gh, out)
+        np.testing.assert_allclose(out, ref.xs[i], rtol=0, atol=1e-12 * np.linalg.norm(ref.xs[i]))
+        xh = out
+
+
+def test_deterministic_bitwise():
+    n, m = 300007, 10
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    r1 = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, "icwy", 15, stats_every=False)
+    r2 = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, "icwy", 15, stats_every=False)
+    for a, b_ in zip(r1.xs, r2.xs):
+        assert np.array_equal(a, b_)
+
+
+def test_fill_uniform_bitwise_equals_host_generator():
+    import aa_inputs
+    n = 1000003
+    t = torch.empty(n, dtype=torch.float64, device="cuda")
+    aa.aa_fill_uniform(t, n, -0.9, 0.9, stream_id=1, offset=12345)
+    torch.cuda.synchronize()
+    h = aa_inputs.uniform(n, -0.9, 0.9, stream=1, offset=12345)
+    assert np.array_equal(t.cpu().numpy(), h)
+
+
+def test_reset_restarts_window(config1):
+    M, b, Gn, Gt = config1
+    s = aa.AndersonSolver(1000, 5, "cgs2", stream=torch.cuda.current_stream())
+    x = torch.zeros(1000, dtype=torch.float64, device="cuda")
+    xn = torch.empty_like(x)
+    s.init(x, Gt(x), xn)
+    x, xn = xn, x
+    for _ in range(7):
+        s.step(x, Gt(x), xn)
+        x, xn = xn, x
+    s.reset()
+    assert s.stats().m_i == 0
+    s.step(x, Gt(x), xn)
+    st = s.stats()
+    assert st.m_i == 1 and st.logical_last["qradd"] == 1
