@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the AA hot path (one Anderson iteration: QRDelete + QRAdd + LSP + update).
+
+Metric (BASELINE.json): "µs per AA iteration (QRAdd+LSP+update) and % HBM roofline at
+1/2/4/8 B200".  A step is one RECYCLE aa_step (window full: Givens QRDelete fused with
+QRAdd, gamma, x update) on config 2 (n_local = 1e8 fp64, m = 20), G(x) = d*x + b
+evaluated by the caller outside the timed region.  Headline variant: DCGS-2; the other
+variants are reported under "variants".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--m 20] [--n-local 1e8]
+                    [--variant dcgs2] [--impl reference] [--sweep] [--no-e2e] [--no-cpu]
+
+N > 1: launched by torchrun; each rank owns n_local rows (weak scaling); the reported
+time is the max over ranks of the CUDA-event time; each global reduction is one
+ncclAllReduce issued by libaa.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "µs per AA iteration (QRAdd+LSP+update) and % HBM roofline at 1/2/4/8 B200"
+VARIANTS = ("dcgs2", "icwy", "cgs2", "mgs")
+
+
+# --------------------------------------------------------------------- byte model
+def k1_bytes(m, V, recycle=True):
+    """K1 (a1 + a2 + a3): reads x, g, f_prev, g_prev + m columns; writes f_prev, g_prev,
+    Delta g, Delta f + the m-1 rotated columns: (2m+7) V at recycle."""
+    return (2 * m + 7) * V if recycle else None
+
+
+def step_bytes(variant, m, V, beta_on=False):
+    """Algorithmic bytes of one RECYCLE aa_step (DESIGN.md §Byte model)."""
+    k = m - 1
+    k1 = (2 * m + 7) * V
+    k4 = (m + 3) * V
+    if variant == "dcgs2":
+        k2 = (k + 4) * V if k >= 3 else (k + 3) * V
+    elif variant == "icwy":
+        k2 = (k + 3) * V
+    elif variant == "cgs2":
+        k2 = (k + 2) * V + (k + 3) * V
+    else:
+        k2 = 4 * V * k
+    return k1 + k2 + k4
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def read_traffic(variant, m):
+    """dram__bytes_read.sum + dram__bytes_write.sum per K1 launch from the committed ncu
+    --set full summary (profiles/), if one exists for this configuration."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        e = s.get("k1", {}).get(f"{variant}_m{m}")
+        return float(e["dram_bytes_per_launch"]) if e else None
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------- clocks sampler
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=3)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- oracle baseline
+def oracle_sample(m, variant, n_sample, steps, warmup, n_target):
+    """Time O2 (numpy fp64, the paper's incremental QR) per RECYCLE iteration on the host
+    cores at n_sample rows, scaled linearly (bandwidth-bound) to n_target."""
+    from aa_inputs import problems
+    from oracle import aa_variant
+    d, b = problems.diagonal(n_sample)
+    G = lambda x: d * x + b
+    times = []
+    t_last = [time.perf_counter()]
+
+    def G_timed(x):
+        now = time.perf_counter()
+        times.append(now - t_last[0])
+        out = G(x)
+        t_last[0] = time.perf_counter()
+        return out
+
+    # run start-up + warmup + steps; the time between consecutive G calls is one AA
+    # iteration of the oracle (G itself excluded)
+    aa_variant(G_timed, np.zeros(n_sample), m, variant, m + warmup + steps + 1, record_x=False,
+               record_loo=False)
+    it_times = times[2 + m + warmup: 2 + m + warmup + steps]
+    per_iter = float(np.mean(it_times)) if it_times else float("nan")
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return per_iter * (n_target / n_sample) * 1e6, cores, per_iter * 1e6
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n_target = int(args.n_local)
+    n_sample = int(args.ref_n)
+    us, cores, raw = oracle_sample(args.m, args.variant, n_sample, args.steps, args.warmup, n_target)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": us, "unit": "us/iter", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(args),
+        "cpu_baseline": {"value": us, "unit": "us/iter", "cores": cores, "kind": "oracle",
+                         "sample": f"O2 numpy fp64 {args.variant} m={args.m}: {args.warmup} warm-up + "
+                                   f"{args.steps} timed recycle iterations at n={n_sample} after {args.m} "
+                                   f"start-up ones ({raw:.0f} us/iter), scaled x{n_target / n_sample:g} "
+                                   f"to n_local={n_target} (bandwidth-bound)"},
+        "e2e": {"value": us, "unit": "us/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(args):
+    return {"workload": (f"config2 kernel study: n_local={int(args.n_local)} fp64 rows per GPU, m={args.m}, "
+                         f"{args.variant.upper()} RECYCLE aa_step (QRDelete+QRAdd+LSP+update), "
+                         "G(x)=d*x+b, d~U[-0.9,0.9), b~U[-1,1) (SplitMix64 seed 9667), x0=0"),
+            "n_local": int(args.n_local), "m": args.m, "variant": args.variant,
+            "parallelism": f"rows{args.gpus}", "l2": "inputs larger than L2 (0.8 GB per vector)",
+            "timed": "aa_step only (CUDA events on the handle's stream); G excluded"}
+
+
+# --------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--m", type=int, default=20)
+    ap.add_argument("--n-local", type=float, default=1e8)
+    ap.add_argument("--variant", default="dcgs2", choices=VARIANTS)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--ref-n", type=float, default=1e6)
+    ap.add_argument("--sweep", action="store_true", help="also sweep m in {5,10,20,50} x variants")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--only-headline", action="store_true")
+    ap.add_argument("--icwy-merged", type=int, default=0)
+    args = ap.parse_args()
+    args.steps = max(1, args.steps)
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2110_09667_b200 import aa
+
+    uid = None
+    if world > 1:
+        obj = [aa.aa_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    n_local = int(args.n_local)
+    offset = rank * n_local
+    stream = torch.cuda.current_stream()
+    d = torch.empty(n_local, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(d)
+    aa.aa_fill_uniform(d, n_local, -0.9, 0.9, stream_id=1, offset=offset, stream=stream)
+    aa.aa_fill_uniform(b, n_local, -1.0, 1.0, stream_id=2, offset=offset, stream=stream)
+    G = lambda x: torch.addcmul(b, d, x)
+    peak, peak_src = read_peaks()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def measure(variant, m, steps, warmup, with_clocks=False, e2e=False):
+        s = aa.AndersonSolver(n_local, m, variant, rank=rank, nranks=world, unique_id=uid,
+                              stream=stream, profile=1, n_global=n_local * world,
+                              icwy_merged=args.icwy_merged)
+        x = torch.zeros(n_local, dtype=torch.float64, device="cuda")
+        xn = torch.empty_like(x)
+        s.init(x, G(x), xn)
+        x, xn = xn, x
+        for _ in range(m + warmup):          # fill the window, then warm-up recycle steps
+            s.step(x, G(x), xn)
+            x, xn = xn, x
+        aa.aa_timings(s.h, reset=True)
+        clk = Clocks(local_rank) if with_clocks else None
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        barrier()
+        if clk:
+            clk.start()
+            time.sleep(0.3)
+        l0 = aa.aa_kernel_launches(s.h)
+        for i in range(steps):
+            g = G(x)
+            ev[i][0].record(stream)
+            s.step(x, g, xn)
+            ev[i][1].record(stream)
+            x, xn = xn, x
+        barrier()
+        launches = aa.aa_kernel_launches(s.h) - l0
+        clocks = clk.stop() if clk else None
+        step_ms = [a.elapsed_time(b_) for a, b_ in ev]
+        ms_t, cnt = aa.aa_timings(s.h, reset=True)
+        st = s.stats()
+        res = {"ms_per_step": max_over_ranks(float(np.mean(step_ms))),
+               "ms_min": max_over_ranks(float(np.min(step_ms))),
+               "k1_ms": max_over_ranks(ms_t[0] / max(cnt[0], 1)),
+               "k2_ms_per_step": max_over_ranks(ms_t[1] / steps),
+               "k4_ms": max_over_ranks(ms_t[2] / max(cnt[2], 1)),
+               "allreduce_ms_per_step": max_over_ranks(ms_t[3] / steps),
+               "launches_per_step": launches / steps, "launches": launches,
+               "sync_points_per_step": st.sync_points_last, "allreduce_per_step": st.allreduce_last,
+               "f_norm": st.f_norm}
+        e2e_res = None
+        if e2e:
+            nh = 3
+            xh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+            gh = torch.empty_like(xh)
+            outh = torch.empty_like(xh)
+            dh, bh = d.cpu(), b.cpu()
+            xh.copy_(x.cpu())
+            t_e = []
+            for _ in range(nh):
+                torch.addcmul(bh, dh, xh, out=gh)    # caller's G on the host (untimed)
+                barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                s.step_host(xh, gh, outh)
+                e1.record(stream)
+                barrier()
+                t_e.append(e0.elapsed_time(e1))
+                xh, outh = outh, xh
+            e2e_res = {"value": max_over_ranks(float(np.mean(t_e))) * 1e3, "unit": "us/iter",
+                       "h2d_bytes_per_step": 2 * 8 * n_local, "d2h_bytes_per_step": 8 * n_local,
+                       "steps": nh, "path": "aa_step_host (pinned host x_i, G(x_i) in; x_{i+1} out)"}
+        s.close()
+        del x, xn
+        torch.cuda.empty_cache()
+        return res, clocks, e2e_res
+
+    V = 8 * n_local
+    head, clocks, e2e = measure(args.variant, args.m, args.steps, args.warmup, with_clocks=True,
+                                e2e=not args.no_e2e)
+    variants = {}
+    if not args.only_headline:
+        for v in VARIANTS:
+            if v == args.variant:
+                r = head
+            else:
+                r, _, _ = measure(v, args.m, max(3, args.steps // 2), 3)
+            bytes_step = step_bytes(v, args.m, V)
+            variants[v] = {"us_per_iter": r["ms_per_step"] * 1e3,
+                           "step_hbm_frac": bytes_step / (r["ms_per_step"] * 1e-3) / (peak * 1e9),
+                           "k1_frac": k1_bytes(args.m, V) / (r["k1_ms"] * 1e-3) / (peak * 1e9),
+                           "sync_points": r["sync_points_per_step"], "allreduces": r["allreduce_per_step"],
+                           "launches": r["launches_per_step"]}
+    sweep = {}
+    if args.sweep:
+        for m in (5, 10, 20, 50):
+            for v in VARIANTS:
+                r, _, _ = measure(v, m, 3, 3)
+                sweep[f"{v}_m{m}"] = {"us_per_iter": r["ms_per_step"] * 1e3,
+                                      "step_hbm_frac": step_bytes(v, m, V) / (r["ms_per_step"] * 1e-3) / (peak * 1e9),
+                                      "k1_frac": k1_bytes(m, V) / (r["k1_ms"] * 1e-3) / (peak * 1e9)}
+
+    k1b = k1_bytes(args.m, V)
+    achieved = k1b / (head["k1_ms"] * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": "aa_stream_kernel<OP_K1> (prologue + streaming Givens QRDelete + block multi-dot)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": read_traffic(args.variant, args.m), "peak_source": peak_src,
+            "bytes_per_launch": k1b, "k1_ms": head["k1_ms"],
+            "step_bytes": step_bytes(args.variant, args.m, V),
+            "step_frac": step_bytes(args.variant, args.m, V) / (head["ms_per_step"] * 1e-3) / (peak * 1e9),
+            "k1_share_of_step": head["k1_ms"] / head["ms_per_step"]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        us, cores, raw = oracle_sample(args.m, args.variant, int(args.ref_n), 3, 1, n_local)
+        cpu = {"value": us, "unit": "us/iter", "cores": cores, "kind": "oracle",
+               "sample": f"O2 numpy fp64 {args.variant} m={args.m}: 3 recycle iterations at n={int(args.ref_n)} "
+                         f"({raw:.0f} us/iter) scaled x{n_local / args.ref_n:g} to n_local={n_local}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": head["ms_per_step"] * 1e3, "unit": "us/iter", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": _config(args), "roofline": roof, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": head["launches"], "clocks": clocks,
+                "detail": {k_: v_ for k_, v_ in head.items() if k_ not in ("launches",)},
+                "variants": variants}
+        if sweep:
+            line["sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -3,6 +3,7 @@
 // path of arXiv 2110.09667.  P:n = PAPER.md line n.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace aa {
@@ -65,7 +66,20 @@ struct K1Layout {
   }
 };
 
-struct KParams {
+constexpr int NVEC_MAX = 8;   // 1-D vector streams per kernel
+constexpr int NBLK_MAX = 3;   // 2-D column blocks (tensor maps) per kernel
+
+// Kernel parameters.  Inputs of one tile are staged in shared memory as columns:
+// first the nvec vectors (1-D bulk copies), then the nblk column blocks (one 2-D
+// tensor-map TMA each, box = TR rows x blk_ncols columns).  Column c of a stage
+// lives at stage + c*TR.
+struct alignas(64) KParams {
+  CUtensorMap tm[NBLK_MAX];   // 2-D maps over Q or the Delta G ring (rows x m columns)
+  int blk_gcol[NBLK_MAX];     // first global column of each block
+  int blk_ncols[NBLK_MAX];
+  int nblk, nvec;
+  const double* vec[NVEC_MAX];
+  unsigned exact_vec;         // bit i: vec[i] is a caller buffer (exactly n rows)
   int op, variant, flags;
   int m;            // window capacity
   int k;            // existing columns after QRDelete (new column index)
@@ -80,12 +94,11 @@ struct KParams {
   int final_slot;   // reduction slot holding (||v'||^2, v'^T f)
   int red_slot;     // slot this kernel writes
   int words;        // words this kernel reduces
-  int nin, tr, str, stages;
+  int nin, tr, stages;
+  int vb;           // first vector column (= sum of block columns)
   int beta_on;
   long long n;      // local rows
   double beta, eps_a;
-  const double* in[NIN_MAX];
-  unsigned long long exact[3];   // bit i: input i is a caller buffer (exactly n rows)
   double* Q;        // Q base (column j at Q + j*ld)
   long long ld;
   double* fp;       // f_{i-1} -> f_i
@@ -133,6 +146,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA 2-D tensor copy global -> shared (box at coordinates {row, col}); rows past the
+// tensor's extent are zero-filled.
+__device__ __forceinline__ void tma_2d_g2s(void* dst, const CUtensorMap* map, int row, int col, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(smem_u32(bar))
       : "memory");
 }
 // fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col)

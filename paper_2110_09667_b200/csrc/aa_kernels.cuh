@@ -1,23 +1,32 @@
 // aa_kernels.cuh — the streaming kernels of libaa (sm_100a).
 //
-// One templated persistent kernel per op.  Every op is a pass over row tiles of
-// TR rows: a single thread issues TMA 1-D bulk copies (cp.async.bulk, completion on
-// an mbarrier) of the op's input columns for the tile into a ring of shared-memory
-// stages; all threads then run the op's row-wise work (phase A) out of shared memory
-// and, where the op needs many dot products, a block multi-dot over the staged tile
-// (phase B: lane = row, warp = column set, or fp64 DMMA for Gram blocks).  Per-CTA
-// partial sums are reduced across CTAs in a fixed order by the last CTA to finish
-// (deterministic), which also commits the replicated small factors.
+// One templated persistent kernel per op.  Every op is a pass over row tiles of TR
+// rows.  The op's inputs are staged in a ring of shared-memory stages by TMA: column
+// blocks of Q or of the Delta G ring with ONE 2-D tensor-map copy per block per tile,
+// and plain vectors (x_i, G(x_i), f_{i-1}, G(x_{i-1})) with 1-D bulk copies; the copies
+// of a tile are spread over the warps (lane 0 of warp w issues copies w, w+8, ...)
+// because one issuing thread sustains only ~1 copy per ~150 cycles
+// (tools/stream_bench.cu).  All threads then run the op's row-wise work (phase A) out
+// of shared memory and, where the op needs many dot products, a block multi-dot over
+// the staged tile (phase B: lane = row, warp = column set, templated on the number of
+// columns per warp; or fp64 DMMA 8x8x4 for the Gram blocks of ICWY's T rebuild).
+// Per-CTA partial sums are reduced across CTAs in a fixed order by the last CTA to
+// finish (deterministic), which also commits the replicated small factors.
 //
 // Small-factor work (K3: Givens on R, T^{-1}, back-substitution) is recomputed at the
 // head of every CTA from the replicated state and the latest allreduce results, so no
 // extra launch and no device->host copy is needed between reductions.
+//
+// Stage layout: [block 0][block 1][block 2][vectors], column c at stage + c*TR.
+// Blocks start at 128-byte aligned addresses (TMA tensor copies need it).  Kernels with
+// a Gram use TR in {252,124,60,28}: TR*8 bytes = 24 banks (mod 32) per column, so the
+// 8-column x 4-row DMMA fragment loads are conflict-free.
 #pragma once
 #include "aa_device.cuh"
 
 namespace aa {
 
-constexpr int MAXSTAGES = 8;
+constexpr int MAXSTAGES = 4;
 
 struct HeadArea {
   double coef[NIN_MAX];
@@ -71,7 +80,7 @@ struct K4Head {
 
 // Everything Alg. 2 does after the reductions: the new R column per variant, R_kk,
 // Q^T f_i (merged into the existing reductions; A14), gamma by
-// back-substitution.  Writes Rw (K x K), Tw (ICWY), gamma/coef into H, c into cvec.
+// back-substitution.  Writes Rw (K x K), Tw (ICWY), gamma into H.coef, c into cvec.
 __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   const int lane = threadIdx.x & 31;
   double* Rw = scratch;
@@ -169,19 +178,19 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
     if (p.recycle) k3_givens_delete(p.st->R, p.c_in, scratch, H.cs, H.sn);
     for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->scale[j];
     if (lane == 0) {
-      const int qb = (p.flags & F_DELETE_ONLY) ? 0 : 4;
       if (p.flags & F_DELETE_ONLY) {
         H.na = 0;
         H.nr = 0;
       } else {
+        const int vb = p.vb;
         H.na = k + 2;
-        for (int a = 0; a < k; ++a) H.lcol[a] = qb + a;
-        H.lcol[k] = 0;       // f_i
-        H.lcol[k + 1] = 1;   // Delta f
+        for (int a = 0; a < k; ++a) H.lcol[a] = a;
+        H.lcol[k] = vb;          // f_i
+        H.lcol[k + 1] = vb + 1;  // Delta f
         H.nr = 3;
-        H.rcol[0] = 1;
-        H.rcol[1] = 0;
-        H.rcol[2] = (k >= 1) ? qb + k - 1 : 0;
+        H.rcol[0] = vb + 1;
+        H.rcol[1] = vb;
+        H.rcol[2] = (k >= 1) ? k - 1 : vb;
       }
     }
   } else if constexpr (OP == OP_K2_ICWY) {
@@ -233,33 +242,50 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
 }
 
 // ---------------------------------------------------------------------------- producer
-__device__ __forceinline__ bool is_exact(const KParams& p, int i) {
-  return (p.exact[i >> 6] >> (i & 63)) & 1ull;
+__device__ __forceinline__ uint32_t vec_bytes(const KParams& p, int i, int rows) {
+  return ((p.exact_vec >> i) & 1u) ? (((uint32_t)rows * 8u) & ~15u) : (uint32_t)align_up((size_t)rows * 8u, 16);
 }
 
-__device__ void issue_tile(const KParams& p, double* stage, uint64_t* bar, long long row0, int rows) {
+// Copies of one tile: blocks 0..nblk-1 (one 2-D tensor copy each, full box incl. the
+// zero-filled rows past n), then vectors; lane 0 of warp w issues copies w, w+NWARP, ...
+__device__ void issue_tile_part(const KParams& p, double* stage, uint64_t* bar, long long row0, int rows,
+                                int warp) {
+  const int TR = p.tr;
+  const int ncp = p.nblk + p.nvec;
   uint32_t total = 0;
-  for (int i = 0; i < p.nin; ++i) {
-    uint32_t b = is_exact(p, i) ? ((uint32_t)rows * 8u) & ~15u : (uint32_t)align_up((size_t)rows * 8u, 16);
-    total += b;
-  }
+  for (int c = warp; c < ncp; c += NWARP)
+    total += (c < p.nblk) ? (uint32_t)TR * p.blk_ncols[c] * 8u : vec_bytes(p, c - p.nblk, rows);
   mbar_arrive_expect_tx(bar, total);
-  for (int i = 0; i < p.nin; ++i) {
-    uint32_t b = is_exact(p, i) ? ((uint32_t)rows * 8u) & ~15u : (uint32_t)align_up((size_t)rows * 8u, 16);
-    if (b) bulk_g2s(stage + (size_t)i * p.str, p.in[i] + row0, b, bar);
+  for (int c = warp; c < ncp; c += NWARP) {
+    if (c < p.nblk) {
+      int col0 = 0;
+      for (int b = 0; b < c; ++b) col0 += p.blk_ncols[b];
+      tma_2d_g2s(stage + (size_t)col0 * TR, &p.tm[c], (int)row0, p.blk_gcol[c], bar);
+    } else {
+      const int i = c - p.nblk;
+      const uint32_t b = vec_bytes(p, i, rows);
+      if (b) bulk_g2s(stage + (size_t)(p.vb + i) * TR, p.vec[i] + row0, b, bar);
+    }
   }
 }
 
-// value of input column i at tile row r (falls back to a plain load for the odd last
-// row of a caller buffer that the 16-byte-granular bulk copy could not cover)
-__device__ __forceinline__ double ldS(const KParams& p, const double* S, int i, int r, int rows,
+// value of vector i at tile row r (falls back to a plain load for the odd last row of a
+// caller buffer that the 16-byte-granular bulk copy could not cover)
+__device__ __forceinline__ double ldV(const KParams& p, const double* S, int i, int r, int rows,
                                       long long grow) {
-  if ((rows & 1) && r == rows - 1 && is_exact(p, i)) return p.in[i][grow];
-  return S[(size_t)i * p.str + r];
+  if ((rows & 1) && r == rows - 1 && ((p.exact_vec >> i) & 1u)) return p.vec[i][grow];
+  return S[(size_t)(p.vb + i) * p.tr + r];
+}
+
+__device__ __forceinline__ int gram_block_I(int blk) {
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= blk) ++I;
+  return I;
 }
 
 // ---------------------------------------------------------------------------- kernel
-template <int OP>
+// OP: the op; NCW: phase-B columns per warp (0 = no block multi-dot); GRAM: DMMA Gram.
+template <int OP, int NCW, bool GRAM>
 __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
@@ -269,58 +295,66 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long n = p.n;
-  const int TR = p.tr, STR = p.str, NS = p.stages;
-  const size_t stage_words = (size_t)p.nin * STR;
+  const int TR = p.tr, NS = p.stages;
+  const size_t stage_words = align_up((size_t)p.nin * TR, 16);
   const long long ntiles = (n + TR - 1) / TR;
   const int k = p.k;
+  const int vb = p.vb;
 
   if (warp == 0) op_head<OP>(p, H, scratch);
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], NWARP);
     fence_mbar_init();
   }
   __syncthreads();
 
   const long long my_count =
       (ntiles > (long long)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (tid == 0) {
+  if (lane == 0) {
     fence_proxy_async();
     for (int s = 0; s < NS && s < my_count; ++s) {
       const long long t = blockIdx.x + (long long)s * gridDim.x;
       const long long r0 = t * TR;
-      issue_tile(p, stage0 + s * stage_words, &bars[s], r0, (int)min((long long)TR, n - r0));
+      issue_tile_part(p, stage0 + s * stage_words, &bars[s], r0, (int)min((long long)TR, n - r0), warp);
     }
   }
 
   // phase-A accumulators (row-wise dots / norms)
   double a0 = 0.0, a1 = 0.0;
-  // phase-B accumulators (block multi-dot): warp's columns x up to 3 right-hand sides
-  constexpr int NRB = (OP == OP_K1) ? 3 : (OP == OP_K2A_CGS2 ? 1 : 0);
-  constexpr int NCB = (NRB > 0) ? PB_COLS_PER_WARP : 1;
-  double acc[NCB][NRB > 0 ? NRB : 1];
+  // phase-B accumulators: this warp's NCW columns x NRB right-hand sides
+  constexpr int NRB = (OP == OP_K1) ? 3 : 1;
+  constexpr int NCWx = NCW > 0 ? NCW : 1;
+  double acc[NCWx][NRB];
+  int coff[NCWx], roff[NRB];
 #pragma unroll
-  for (int c = 0; c < NCB; ++c)
+  for (int c = 0; c < NCWx; ++c) {
 #pragma unroll
-    for (int b = 0; b < (NRB > 0 ? NRB : 1); ++b) acc[c][b] = 0.0;
+    for (int b = 0; b < NRB; ++b) acc[c][b] = 0.0;
+    const int a = warp + c * NWARP;
+    coff[c] = (NCW > 0 && a < H.na) ? H.lcol[a] * TR : 0;
+  }
+#pragma unroll
+  for (int b = 0; b < NRB; ++b) roff[b] = (NCW > 0 && b < H.nr) ? H.rcol[b] * TR : 0;
   // Gram accumulators (fp64 DMMA 8x8 blocks): up to 5 blocks per warp
-  constexpr bool HAS_GRAM = (OP == OP_K1 || OP == OP_GRAM);
-  constexpr int GB = HAS_GRAM ? 5 : 1;
+  constexpr int GB = GRAM ? 5 : 1;
   double gc0[GB], gc1[GB];
-#pragma unroll
-  for (int g = 0; g < GB; ++g) gc0[g] = gc1[g] = 0.0;
-  const int kg = (OP == OP_GRAM) ? p.c_in : ((p.flags & F_DELETE_ONLY) ? p.c_in - 1 : k);
-  const int gbase = (OP == OP_GRAM || (p.flags & F_DELETE_ONLY)) ? 0 : 4;
+  int gofa[GB], gofb[GB];
+  const bool del_only = p.flags & F_DELETE_ONLY;
+  const int kg = (OP == OP_GRAM) ? p.c_in : (del_only ? p.c_in - 1 : k);
   const int nb8 = (kg + 7) / 8;
-  const int nblk = nb8 * (nb8 + 1) / 2;
-  const bool do_gram = HAS_GRAM && p.gram != 0 && (OP == OP_GRAM ? kg >= 1 : kg >= 2);
-  int gI[GB], gJ[GB];
+  const int nblk8 = nb8 * (nb8 + 1) / 2;
+  const bool do_gram = GRAM && p.gram != 0 && (OP == OP_GRAM ? kg >= 1 : kg >= 2);
+  {
+    const int g_r = lane >> 2, g_c = lane & 3;
 #pragma unroll
-  for (int g = 0; g < GB; ++g) {
-    const int blk = warp + g * NWARP;
-    int I = 0;
-    while ((I + 1) * (I + 2) / 2 <= blk) ++I;
-    gI[g] = I;
-    gJ[g] = blk - I * (I + 1) / 2;
+    for (int g = 0; g < GB; ++g) {
+      gc0[g] = gc1[g] = 0.0;
+      const int blk = warp + g * NWARP;
+      const int I = gram_block_I(blk), J = blk - I * (I + 1) / 2;
+      const int ca = 8 * I + g_r, cb = 8 * J + g_r;
+      gofa[g] = (ca < kg) ? ca * TR + g_c : -1;   // columns past kg contribute 0
+      gofb[g] = (cb < kg) ? cb * TR + g_c : -1;
+    }
   }
 
   for (long long it = 0; it < my_count; ++it) {
@@ -337,101 +371,113 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     if (r < TR) {
       const long long grow = row0 + r;
       if constexpr (OP == OP_K1) {
-        const bool del_only = p.flags & F_DELETE_ONLY;
-        const int qb = del_only ? 0 : 4;
         const int ncols = del_only ? p.c_in : (p.recycle ? p.c_in : k);
         if (r < rows) {
           double f = 0.0, df = 0.0;
           if (!del_only) {
             if (p.flags & F_EXT_DF) {
-              df = ldS(p, S, 0, r, rows, grow);
+              df = ldV(p, S, 0, r, rows, grow);
               f = df;
             } else {
               // Alg. 1 l.3-5: f_i = G(x_i) - x_i, Delta f = f_i - f_{i-1}, Delta g = G(x_i) - G(x_{i-1})
-              const double x = ldS(p, S, 0, r, rows, grow);
-              const double g = ldS(p, S, 1, r, rows, grow);
-              const double fpv = S[2 * (size_t)STR + r];
-              const double gpv = S[3 * (size_t)STR + r];
+              const double x = ldV(p, S, 0, r, rows, grow);
+              const double g = ldV(p, S, 1, r, rows, grow);
+              const double fpv = S[(size_t)(vb + 2) * TR + r];
+              const double gpv = S[(size_t)(vb + 3) * TR + r];
               f = g - x;
               df = f - fpv;
-              const double dg = g - gpv;
               p.fp[grow] = f;
               p.gp[grow] = g;
-              p.dg_out[grow] = dg;
+              p.dg_out[grow] = g - gpv;
             }
           }
           if (p.recycle) {
             // QRDelete on Q: streaming carry form of the m-1 Givens rotations of adjacent
             // column pairs; the last carry is the dropped column.
-            double carry = S[(size_t)qb * STR + r] * H.sc[0];
+            double carry = S[r] * H.sc[0];
+#pragma unroll 4
             for (int j = 0; j < p.c_in - 1; ++j) {
-              const double qn = S[(size_t)(qb + j + 1) * STR + r] * H.sc[j + 1];
+              const double qn = S[(size_t)(j + 1) * TR + r] * H.sc[j + 1];
               const double c = H.cs[j], s = H.sn[j];
-              const double out = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s, qn));
-              carry = __dadd_rn(__dmul_rn(-s, carry), __dmul_rn(c, qn));
-              S[(size_t)(qb + j) * STR + r] = out;
+              const double out = fma(c, carry, s * qn);
+              carry = fma(-s, carry, c * qn);
+              S[(size_t)j * TR + r] = out;
               p.Q[(size_t)j * p.ld + grow] = out;
             }
           } else {
-            for (int j = 0; j < ncols; ++j) S[(size_t)(qb + j) * STR + r] *= H.sc[j];
+            for (int j = 0; j < ncols; ++j) S[(size_t)j * TR + r] *= H.sc[j];
           }
           if (!del_only) {
             p.Q[(size_t)k * p.ld + grow] = df;  // unnormalised new column (lazy scale)
-            S[r] = f;
-            S[(size_t)STR + r] = df;
+            S[(size_t)vb * TR + r] = f;
+            S[(size_t)(vb + 1) * TR + r] = df;
           }
-        } else {
-          if (!del_only) {
-            S[r] = 0.0;
-            S[(size_t)STR + r] = 0.0;
-          }
-          for (int j = 0; j < ncols; ++j) S[(size_t)(qb + j) * STR + r] = 0.0;
+        } else if (!del_only) {
+          // Q block rows past n are zero-filled by the tensor copy
+          S[(size_t)vb * TR + r] = 0.0;
+          S[(size_t)(vb + 1) * TR + r] = 0.0;
         }
       } else if constexpr (OP == OP_K2_ICWY || OP == OP_K2B_CGS2) {
         // ICWY: Alg. 4 l.5  Delta f - Q (T^{-1} r);  CGS-2: Alg. 5 l.4  y - Q z
         if (r < rows) {
-          double v = S[(size_t)k * STR + r];
-#pragma unroll 4
-          for (int j = 0; j < k; ++j) v -= H.coef[j] * S[(size_t)j * STR + r];
+          double v0 = S[(size_t)k * TR + r], v1 = 0.0;
+          int j = 0;
+#pragma unroll 2
+          for (; j + 1 < k; j += 2) {
+            v0 -= H.coef[j] * S[(size_t)j * TR + r];
+            v1 -= H.coef[j + 1] * S[(size_t)(j + 1) * TR + r];
+          }
+          if (j < k) v0 -= H.coef[j] * S[(size_t)j * TR + r];
+          const double v = v0 + v1;
           p.Q[(size_t)k * p.ld + grow] = v;
           a0 += v * v;
-          a1 += v * S[(size_t)(k + 1) * STR + r];
+          a1 += v * S[(size_t)(k + 1) * TR + r];
         }
       } else if constexpr (OP == OP_K2_DCGS2) {
         if (r < rows) {
           // Alg. 6 l.4 (reading A1): q_{k-1} <- q_{k-1} - Q_{0:k-2} s
-          double qn = S[(size_t)(k - 1) * STR + r] * H.sc[k - 1];
+          double qn = S[(size_t)(k - 1) * TR + r] * H.sc[k - 1];
+          double v1 = 0.0;
           if (p.reortho) {
 #pragma unroll 4
-            for (int j = 0; j < k - 1; ++j) qn -= H.coef2[j] * S[(size_t)j * STR + r];
+            for (int j = 0; j < k - 1; ++j) {
+              const double qj = S[(size_t)j * TR + r];
+              qn -= H.coef2[j] * qj;
+              v1 -= H.coef[j] * qj;
+            }
             p.Q[(size_t)(k - 1) * p.ld + grow] = qn;
+          } else {
+#pragma unroll 4
+            for (int j = 0; j < k - 1; ++j) v1 -= H.coef[j] * S[(size_t)j * TR + r];
           }
           // Alg. 6 l.7: Delta f <- Delta f - Q_{0:k-1} R_{0:k-1,k}
-          double v = S[(size_t)k * STR + r];
-#pragma unroll 4
-          for (int j = 0; j < k - 1; ++j) v -= H.coef[j] * S[(size_t)j * STR + r];
-          v -= H.coef[k - 1] * qn;
+          const double v = (S[(size_t)k * TR + r] - H.coef[k - 1] * qn) + v1;
           p.Q[(size_t)k * p.ld + grow] = v;
           a0 += v * v;
-          a1 += v * S[(size_t)(k + 1) * STR + r];
+          a1 += v * S[(size_t)(k + 1) * TR + r];
         }
       } else if constexpr (OP == OP_K2A_CGS2) {
         if (r < rows) {
-          double v = S[(size_t)k * STR + r];
-#pragma unroll 4
-          for (int j = 0; j < k; ++j) v -= H.coef[j] * S[(size_t)j * STR + r];
+          double v0 = S[(size_t)k * TR + r], v1 = 0.0;
+          int j = 0;
+#pragma unroll 2
+          for (; j + 1 < k; j += 2) {
+            v0 -= H.coef[j] * S[(size_t)j * TR + r];
+            v1 -= H.coef[j + 1] * S[(size_t)(j + 1) * TR + r];
+          }
+          if (j < k) v0 -= H.coef[j] * S[(size_t)j * TR + r];
+          const double v = v0 + v1;
           p.Q[(size_t)k * p.ld + grow] = v;  // y (Alg. 5 l.2), in place
-          S[(size_t)k * STR + r] = v;
-          for (int j = 0; j < k; ++j) S[(size_t)j * STR + r] *= H.sc[j];
-        } else {
-          for (int j = 0; j <= k; ++j) S[(size_t)j * STR + r] = 0.0;
+          S[(size_t)k * TR + r] = v;
+          for (int jj = 0; jj < k; ++jj) S[(size_t)jj * TR + r] *= H.sc[jj];
         }
+        // rows past n: the tensor copy zero-filled every column
       } else if constexpr (OP == OP_K2_MGS) {
         if (r < rows) {
           // Alg. 3 l.3 (column j-1) then l.2 for column j (or the norm, l.5)
-          double v = S[(size_t)STR + r] - H.scal[0] * S[r];
+          const double v = S[(size_t)TR + r] - H.scal[0] * S[r];
           p.Q[(size_t)k * p.ld + grow] = v;
-          const double w = S[2 * (size_t)STR + r];
+          const double w = S[2 * (size_t)TR + r];
           if (p.mgs_j < k) {
             a0 += w * H.scal[1] * v;
           } else {
@@ -442,15 +488,20 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       } else if constexpr (OP == OP_K4) {
         if (r < rows) {
           // Alg. 1 l.7: x_{i+1} = G(x_i) - G_i gamma   [- (1-beta)(f_i - Q Q^T f_i), A13]
-          const double g = ldS(p, S, 0, r, rows, grow);
-          const double x = ldS(p, S, 1, r, rows, grow);
-          double xn = g;
-#pragma unroll 4
-          for (int j = 0; j <= k; ++j) xn -= H.coef[j] * S[(size_t)(2 + j) * STR + r];
+          const double g = ldV(p, S, 0, r, rows, grow);
+          const double x = ldV(p, S, 1, r, rows, grow);
+          double x0 = g, x1 = 0.0;
+          int j = 0;
+#pragma unroll 2
+          for (; j + 1 <= k; j += 2) {
+            x0 -= H.coef[j] * S[(size_t)j * TR + r];
+            x1 -= H.coef[j + 1] * S[(size_t)(j + 1) * TR + r];
+          }
+          if (j <= k) x0 -= H.coef[j] * S[(size_t)j * TR + r];
+          double xn = x0 + x1;
           if (p.beta_on) {
-            const int kf = k + 3;
-            double t = S[(size_t)kf * STR + r];
-            for (int j = 0; j <= k; ++j) t -= H.coef2[j] * S[(size_t)(kf + 1 + j) * STR + r];
+            double t = S[(size_t)(vb + 2) * TR + r];
+            for (int jj = 0; jj <= k; ++jj) t -= H.coef2[jj] * S[(size_t)(k + 1 + jj) * TR + r];
             xn -= H.scal[0] * t;
           }
           p.x_out[grow] = xn;
@@ -458,46 +509,40 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           a0 += d * d;
         }
       } else if constexpr (OP == OP_GRAM) {
-        for (int j = 0; j < p.c_in; ++j) {
-          double& s = S[(size_t)j * STR + r];
-          s = (r < rows) ? s * H.sc[j] : 0.0;
-        }
+        if (r < rows)
+          for (int j = 0; j < p.c_in; ++j) S[(size_t)j * TR + r] *= H.sc[j];
       }
     }
 
     // ------------------------------------------------------------ phase B (multi-dot)
-    if constexpr (NRB > 0 || HAS_GRAM) {
+    if constexpr (NCW > 0 || GRAM) {
       __syncthreads();
-      if constexpr (NRB > 0) {
-        const int na = H.na, nr = H.nr;
-        if (na > 0) {
+      if constexpr (NCW > 0) {
+        if (H.na > 0) {
+#pragma unroll 2
           for (int rr = lane; rr < TR; rr += 32) {
+            const double* Sr = S + rr;
             double rhs[NRB];
 #pragma unroll
-            for (int b = 0; b < NRB; ++b) rhs[b] = (b < nr) ? S[(size_t)H.rcol[b] * STR + rr] : 0.0;
+            for (int b = 0; b < NRB; ++b) rhs[b] = Sr[roff[b]];
 #pragma unroll
-            for (int c = 0; c < NCB; ++c) {
-              const int a = warp + c * NWARP;
-              if (a < na) {
-                const double v = S[(size_t)H.lcol[a] * STR + rr];
+            for (int c = 0; c < NCW; ++c) {
+              const double v = Sr[coff[c]];
 #pragma unroll
-                for (int b = 0; b < NRB; ++b) acc[c][b] += v * rhs[b];
-              }
+              for (int b = 0; b < NRB; ++b) acc[c][b] = fma(v, rhs[b], acc[c][b]);
             }
           }
         }
       }
-      if constexpr (HAS_GRAM) {
+      if constexpr (GRAM) {
         if (do_gram) {
-          const int g_r = lane >> 2, g_c = lane & 3;
           for (int r0 = 0; r0 < TR; r0 += 4) {
+            const double* Sr = S + r0;
 #pragma unroll
             for (int g = 0; g < GB; ++g) {
-              const int blk = warp + g * NWARP;
-              if (blk < nblk) {
-                const int ca = 8 * gI[g] + g_r, cb = 8 * gJ[g] + g_r;
-                const double av = (ca < kg) ? S[(size_t)(gbase + ca) * STR + r0 + g_c] : 0.0;
-                const double bv = (cb < kg) ? S[(size_t)(gbase + cb) * STR + r0 + g_c] : 0.0;
+              if (warp + g * NWARP < nblk8) {
+                const double av = gofa[g] >= 0 ? Sr[gofa[g]] : 0.0;
+                const double bv = gofb[g] >= 0 ? Sr[gofb[g]] : 0.0;
                 dmma_8x8x4(gc0[g], gc1[g], av, bv);
               }
             }
@@ -506,11 +551,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       }
     }
     __syncthreads();
-    if (tid == 0 && it + NS < my_count) {
+    if (lane == 0 && it + NS < my_count) {
       fence_proxy_async();
       const long long t2 = blockIdx.x + (it + NS) * gridDim.x;
       const long long r2 = t2 * TR;
-      issue_tile(p, S, &bars[sidx], r2, (int)min((long long)TR, n - r2));
+      issue_tile_part(p, S, &bars[sidx], r2, (int)min((long long)TR, n - r2), warp);
     }
   }
 
@@ -518,12 +563,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   double* mypart = p.part + (size_t)blockIdx.x * LRED;
   if constexpr (OP == OP_K1) {
     const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
-    const bool del_only = p.flags & F_DELETE_ONLY;
     if (!del_only) {
 #pragma unroll
-      for (int c = 0; c < NCB; ++c) {
+      for (int c = 0; c < NCWx; ++c) {
         const int a = warp + c * NWARP;
-        if (a < H.na) {
+        if (NCW > 0 && a < H.na) {
 #pragma unroll
           for (int b = 0; b < NRB; ++b) {
             const double v = warp_sum(acc[c][b]);
@@ -551,8 +595,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 #pragma unroll
       for (int g = 0; g < GB; ++g) {
         const int blk = warp + g * NWARP;
-        if (blk < nblk) {
-          const int I = gI[g], J = gJ[g];
+        if (blk < nblk8) {
+          const int I = gram_block_I(blk), J = blk - I * (I + 1) / 2;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int i = 8 * I + g_r, j = 8 * J + 2 * g_c + e;
@@ -570,9 +614,9 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   } else if constexpr (OP == OP_K2A_CGS2) {
 #pragma unroll
-    for (int c = 0; c < NCB; ++c) {
+    for (int c = 0; c < NCWx; ++c) {
       const int a = warp + c * NWARP;
-      if (a < H.na) {
+      if (NCW > 0 && a < H.na) {
         const double v = warp_sum(acc[c][0]);
         if (lane == 0) mypart[a] = v;
       }
@@ -583,8 +627,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 #pragma unroll
       for (int g = 0; g < GB; ++g) {
         const int blk = warp + g * NWARP;
-        if (blk < nblk) {
-          const int I = gI[g], J = gJ[g];
+        if (blk < nblk8) {
+          const int I = gram_block_I(blk), J = blk - I * (I + 1) / 2;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int i = 8 * I + g_r, j = 8 * J + 2 * g_c + e;

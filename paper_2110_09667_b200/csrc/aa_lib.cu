@@ -1,6 +1,8 @@
 // aa_lib.cu — libaa host side: the C ABI of include/aa.h and include/aa_testing.h,
 // the per-variant schedule of kernels and allreduces (one ncclAllReduce per global
 // reduction), and the reduction ledger.  P:n = PAPER.md line n.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -8,6 +10,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/aa.h"
@@ -82,6 +86,7 @@ struct aa_ctx {
   int ar_last = 0, sp_last = 0;
   int64_t launches = 0;
   std::vector<TimedEv> evs;
+  std::map<std::tuple<int, int, int>, CUtensorMap> tmaps;  // (buffer, box cols, box rows)
   double t_ms[5] = {0, 0, 0, 0, 0};
   int64_t t_cnt[5] = {0, 0, 0, 0, 0};
 };
@@ -108,11 +113,17 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 double* qcol(aa_ctx* c, int j) { return c->Q + (size_t)j * c->ld; }
 double* dgcol(aa_ctx* c, int slot) { return c->DG + (size_t)slot * c->ld; }
 
-void choose_tile(int nin, int* tr, int* stages) {
-  const size_t budget = 160 * 1024;
-  const int trs[4] = {256, 128, 64, 32};
+// Tile rows / stage count: the largest tile that keeps >= 3 stages within ~200 KB of
+// shared memory (tools/stream_bench.cu: ~7 TB/s at 252-256 rows, 3-4 stages, 1 CTA/SM).
+// Kernels with a DMMA Gram take TR in {252,124,60,28} (bank skew), the others
+// TR in {256,128,64,32} (every 2-D box lands 128-byte aligned).
+void choose_tile(int nin, bool skew, int* tr, int* stages) {
+  const size_t budget = 200 * 1024;
+  const int trs_s[4] = {252, 124, 60, 28};
+  const int trs_p[4] = {256, 128, 64, 32};
+  const int* trs = skew ? trs_s : trs_p;
   for (int t = 0; t < 4; ++t) {
-    const size_t sb = (size_t)nin * (trs[t] + 4) * sizeof(double);
+    const size_t sb = align_up((size_t)nin * trs[t], 16) * sizeof(double);
     int s = (int)std::min<size_t>(MAXSTAGES, budget / sb);
     if (s >= 3) {
       *tr = trs[t];
@@ -120,9 +131,69 @@ void choose_tile(int nin, int* tr, int* stages) {
       return;
     }
   }
-  *tr = 32;
+  *tr = trs[3];
   *stages = 2;
 }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+// 2-D tensor map over a column-major n x m buffer (Q or the Delta G ring), box = tr rows
+// x ncols columns; rows past n read as zero.  Cached per (buffer, ncols, tr).
+const CUtensorMap* get_map(aa_ctx* c, int which, int ncols, int tr) {
+  auto key = std::make_tuple(which, ncols, tr);
+  auto it = c->tmaps.find(key);
+  if (it != c->tmaps.end()) return &it->second;
+  auto fn = encode_fn();
+  if (!fn) return nullptr;
+  CUtensorMap m;
+  cuuint64_t gdim[2] = {(cuuint64_t)c->n, (cuuint64_t)c->m};
+  cuuint64_t gstr[1] = {(cuuint64_t)(c->ld * sizeof(double))};
+  cuuint32_t box[2] = {(cuuint32_t)tr, (cuuint32_t)ncols};
+  cuuint32_t es[2] = {1, 1};
+  void* base = which == 0 ? (void*)c->Q : (void*)c->DG;
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "libaa: cuTensorMapEncodeTiled failed (%d) for %d cols x %d rows\n", (int)r, ncols, tr);
+    return nullptr;
+  }
+  return &(c->tmaps[key] = m);
+}
+
+// Column-block / vector description of a kernel's inputs (before the tile is chosen).
+struct Inputs {
+  int nblk = 0, nvec = 0;
+  int blk_which[NBLK_MAX], blk_gcol[NBLK_MAX], blk_ncols[NBLK_MAX];
+  const double* vec[NVEC_MAX];
+  unsigned exact = 0;
+  void block(int which, int gcol, int ncols) {
+    if (ncols <= 0) return;
+    blk_which[nblk] = which;
+    blk_gcol[nblk] = gcol;
+    blk_ncols[nblk] = ncols;
+    ++nblk;
+  }
+  void vector(const double* v, bool is_exact) {
+    if (is_exact) exact |= 1u << nvec;
+    vec[nvec++] = v;
+  }
+  int ncols() const {
+    int s = 0;
+    for (int b = 0; b < nblk; ++b) s += blk_ncols[b];
+    return s;
+  }
+};
 
 struct EvScope {
   aa_ctx* c;
@@ -144,27 +215,65 @@ struct EvScope {
   }
 };
 
-template <int OP>
-int launch_op(aa_ctx* c, KParams& p, int cls) {
-  int tr, stages;
-  choose_tile(std::max(p.nin, 1), &tr, &stages);
-  p.tr = tr;
-  p.str = tr + 4;
-  p.stages = stages;
-  const size_t stage_bytes = (size_t)stages * std::max(p.nin, 1) * p.str * sizeof(double);
-  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scratch_bytes());
+template <int OP, int NCW, bool G>
+int launch_inst(aa_ctx* c, KParams& p, size_t smem, int cls) {
   static size_t attr_set = 0;
   if (smem > attr_set) {
-    CUDA_TRY(c, cudaFuncSetAttribute(aa_stream_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(c, cudaFuncSetAttribute(aa_stream_kernel<OP, NCW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     attr_set = smem;
   }
   int per_sm = 1;
-  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP>, NT, smem));
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP, NCW, G>, NT, smem));
   per_sm = std::max(1, std::min(per_sm, 2));
-  const long long ntiles = (p.n + tr - 1) / tr;
+  const long long ntiles = (p.n + p.tr - 1) / p.tr;
   long long grid = std::min<long long>(ntiles, (long long)c->sms * per_sm);
   if (grid < 1) grid = 1;
+  {
+    EvScope ev(c, cls);
+    aa_stream_kernel<OP, NCW, G><<<(unsigned)grid, NT, smem, c->stream>>>(p);
+  }
+  c->launches++;
+  CUDA_TRY(c, cudaGetLastError());
+  return AA_OK;
+}
+
+#define AA_NCW_CASES(OP, G)                         \
+  switch (ncw) {                                    \
+    case 1: return launch_inst<OP, 1, G>(c, p, smem, cls); \
+    case 2: return launch_inst<OP, 2, G>(c, p, smem, cls); \
+    case 3: return launch_inst<OP, 3, G>(c, p, smem, cls); \
+    case 4: return launch_inst<OP, 4, G>(c, p, smem, cls); \
+    case 5: return launch_inst<OP, 5, G>(c, p, smem, cls); \
+    case 6: return launch_inst<OP, 6, G>(c, p, smem, cls); \
+    case 7: return launch_inst<OP, 7, G>(c, p, smem, cls); \
+    case 8: return launch_inst<OP, 8, G>(c, p, smem, cls); \
+    default: return launch_inst<OP, 9, G>(c, p, smem, cls); \
+  }
+
+template <int OP>
+int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
+  const bool gram = (OP == OP_GRAM) || (OP == OP_K1 && p.gram != 0);
+  const int nin = in.ncols() + in.nvec;
+  int tr, stages;
+  choose_tile(std::max(nin, 1), gram, &tr, &stages);
+  p.tr = tr;
+  p.stages = stages;
+  p.nin = nin;
+  p.vb = in.ncols();
+  p.nblk = in.nblk;
+  p.nvec = in.nvec;
+  p.exact_vec = in.exact;
+  for (int b = 0; b < in.nblk; ++b) {
+    const CUtensorMap* m = get_map(c, in.blk_which[b], in.blk_ncols[b], tr);
+    if (!m) return fail(c, AA_ERR_CUDA);
+    p.tm[b] = *m;
+    p.blk_gcol[b] = in.blk_gcol[b];
+    p.blk_ncols[b] = in.blk_ncols[b];
+  }
+  for (int i = 0; i < in.nvec; ++i) p.vec[i] = in.vec[i];
+  const size_t stage_bytes = (size_t)stages * align_up((size_t)std::max(nin, 1) * tr, 16) * sizeof(double);
+  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scratch_bytes());
   p.st = c->st;
   p.red = c->red;
   p.part = c->part;
@@ -172,13 +281,21 @@ int launch_op(aa_ctx* c, KParams& p, int cls) {
   p.ld = c->ld;
   p.fp = c->fp;
   p.gp = c->gp;
-  {
-    EvScope ev(c, cls);
-    aa_stream_kernel<OP><<<(unsigned)grid, NT, smem, c->stream>>>(p);
+  if constexpr (OP == OP_K1) {
+    const int ncw = (p.flags & F_DELETE_ONLY) ? 1 : (p.k + 2 + NWARP - 1) / NWARP;
+    if (gram) {
+      AA_NCW_CASES(OP_K1, true)
+    } else {
+      AA_NCW_CASES(OP_K1, false)
+    }
+  } else if constexpr (OP == OP_K2A_CGS2) {
+    const int ncw = std::max(1, (p.k + NWARP - 1) / NWARP);
+    AA_NCW_CASES(OP_K2A_CGS2, false)
+  } else if constexpr (OP == OP_GRAM) {
+    return launch_inst<OP_GRAM, 0, true>(c, p, smem, cls);
+  } else {
+    return launch_inst<OP, 0, false>(c, p, smem, cls);
   }
-  c->launches++;
-  CUDA_TRY(c, cudaGetLastError());
-  return AA_OK;
 }
 
 int allreduce(aa_ctx* c, double* buf, size_t count) {
@@ -194,8 +311,6 @@ int allreduce(aa_ctx* c, double* buf, size_t count) {
   c->ar_total++;
   return AA_OK;
 }
-
-void set_exact(KParams& p, int i) { p.exact[i >> 6] |= (1ull << (i & 63)); }
 
 KParams base_params(aa_ctx* c) {
   KParams p;
@@ -253,25 +368,21 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   {
     KParams q = p;
     q.op = OP_K1;
+    Inputs in;
+    in.block(0, 0, c_in);                 // Q_0 .. Q_{c_in-1}
     if (ext) {
-      for (int i = 0; i < 4; ++i) {
-        q.in[i] = vext;
-        set_exact(q, i);
-      }
+      in.vector(vext, true);              // Delta f supplied by the caller
+      in.vector(vext, true);
     } else {
-      q.in[0] = x;
-      q.in[1] = g;
-      q.in[2] = c->fp;
-      q.in[3] = c->gp;
-      set_exact(q, 0);
-      set_exact(q, 1);
+      in.vector(x, true);
+      in.vector(g, true);
+      in.vector(c->fp, false);
+      in.vector(c->gp, false);
     }
-    for (int j = 0; j < c_in; ++j) q.in[4 + j] = qcol(c, j);
-    q.nin = 4 + c_in;
     q.dg_out = dgcol(c, dg_slot);
     q.words = L.words;
     q.red_slot = 0;
-    RET_IF(launch_op<OP_K1>(c, q, 0));
+    RET_IF(launch_op<OP_K1>(c, q, in, 0));
   }
   if (gram && L.n_gram > 0 && !c->icwy_merged) {
     // the ICWY correction-matrix update after QRDelete: its own reduction
@@ -289,33 +400,33 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     KParams q = p;
     if (V == V_ICWY || V == V_DCGS2) {
       q.op = (V == V_ICWY) ? OP_K2_ICWY : OP_K2_DCGS2;
-      for (int j = 0; j <= k; ++j) q.in[j] = qcol(c, j);
-      q.in[k + 1] = c->fp;
-      q.nin = k + 2;
+      Inputs in;
+      in.block(0, 0, k + 1);              // Q_0 .. Q_{k-1}, Delta f (slot k)
+      in.vector(c->fp, false);            // f_i
       q.words = 2;
       q.red_slot = 1;
-      if (V == V_ICWY) RET_IF(launch_op<OP_K2_ICWY>(c, q, 1));
-      else RET_IF(launch_op<OP_K2_DCGS2>(c, q, 1));
+      if (V == V_ICWY) RET_IF(launch_op<OP_K2_ICWY>(c, q, in, 1));
+      else RET_IF(launch_op<OP_K2_DCGS2>(c, q, in, 1));
       RET_IF(allreduce(c, c->red + LRED, 2));
       c->sp_last++;
       final_slot = 1;
     } else if (V == V_CGS2) {
       q.op = OP_K2A_CGS2;
-      for (int j = 0; j <= k; ++j) q.in[j] = qcol(c, j);
-      q.nin = k + 1;
+      Inputs in;
+      in.block(0, 0, k + 1);
       q.words = k;
       q.red_slot = 1;
-      RET_IF(launch_op<OP_K2A_CGS2>(c, q, 1));
+      RET_IF(launch_op<OP_K2A_CGS2>(c, q, in, 1));
       RET_IF(allreduce(c, c->red + LRED, (size_t)k));
       c->sp_last++;
       KParams q2 = p;
       q2.op = OP_K2B_CGS2;
-      for (int j = 0; j <= k; ++j) q2.in[j] = qcol(c, j);
-      q2.in[k + 1] = c->fp;
-      q2.nin = k + 2;
+      Inputs in2;
+      in2.block(0, 0, k + 1);
+      in2.vector(c->fp, false);
       q2.words = 2;
       q2.red_slot = 2;
-      RET_IF(launch_op<OP_K2B_CGS2>(c, q2, 1));
+      RET_IF(launch_op<OP_K2B_CGS2>(c, q2, in2, 1));
       RET_IF(allreduce(c, c->red + 2 * LRED, 2));
       c->sp_last++;
       final_slot = 2;
@@ -324,13 +435,13 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
         KParams q2 = p;
         q2.op = OP_K2_MGS;
         q2.mgs_j = j;
-        q2.in[0] = qcol(c, j - 1);
-        q2.in[1] = qcol(c, k);
-        q2.in[2] = (j < k) ? qcol(c, j) : c->fp;
-        q2.nin = 3;
+        Inputs in;
+        in.vector(qcol(c, j - 1), false);
+        in.vector(qcol(c, k), false);
+        in.vector((j < k) ? qcol(c, j) : c->fp, false);
         q2.words = (j < k) ? 1 : 2;
         q2.red_slot = j;
-        RET_IF(launch_op<OP_K2_MGS>(c, q2, 1));
+        RET_IF(launch_op<OP_K2_MGS>(c, q2, in, 1));
         RET_IF(allreduce(c, c->red + (size_t)j * LRED, (size_t)q2.words));
         c->sp_last++;
       }
@@ -343,25 +454,23 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     q.op = OP_K4;
     q.final_slot = final_slot;
     q.words = 1;
+    Inputs in;
     if (ext) {
       q.n = 0;
-      q.nin = 0;
       q.flags |= F_COMMIT_ONLY;
     } else {
-      q.in[0] = g;
-      q.in[1] = x;
-      set_exact(q, 0);
-      set_exact(q, 1);
-      for (int j = 0; j <= k; ++j) q.in[2 + j] = dgcol(c, (c->dg_head + j) % c->m);
-      int nin = 2 + (k + 1);
-      if (q.beta_on) {
-        q.in[nin++] = c->fp;
-        for (int j = 0; j <= k; ++j) q.in[nin++] = qcol(c, j);
-      }
-      q.nin = nin;
+      // the Delta G window (oldest first) is a ring: at most two contiguous slot ranges
+      const int first = c->dg_head, cnt = k + 1;
+      const int c1 = std::min(cnt, c->m - first);
+      in.block(1, first, c1);
+      in.block(1, 0, cnt - c1);
+      if (q.beta_on) in.block(0, 0, k + 1);
+      in.vector(g, true);
+      in.vector(x, true);
+      if (q.beta_on) in.vector(c->fp, false);
       q.x_out = xn;
     }
-    RET_IF(launch_op<OP_K4>(c, q, 2));
+    RET_IF(launch_op<OP_K4>(c, q, in, 2));
   }
   c->mi = k + 1;
   // ---------------- ledger (paper's logical counts)
@@ -578,11 +687,11 @@ int aa_delete_oldest(aa_handle_t h) {
   {
     KParams q = p;
     q.op = OP_K1;
-    for (int j = 0; j < h->mi; ++j) q.in[j] = qcol(h, j);
-    q.nin = h->mi;
+    Inputs in;
+    in.block(0, 0, h->mi);
     q.words = words;
     q.red_slot = 0;
-    RET_IF(launch_op<OP_K1>(h, q, 0));
+    RET_IF(launch_op<OP_K1>(h, q, in, 0));
   }
   if (V == V_ICWY) {
     RET_IF(allreduce(h, h->red, (size_t)words));
@@ -592,10 +701,9 @@ int aa_delete_oldest(aa_handle_t h) {
     KParams q = p;
     q.op = OP_K4;
     q.n = 0;
-    q.nin = 0;
     q.words = 1;
     q.flags |= F_COMMIT_ONLY;
-    RET_IF(launch_op<OP_K4>(h, q, 2));
+    RET_IF(launch_op<OP_K4>(h, q, Inputs(), 2));
   }
   h->mi = k;
   h->dg_head = (h->dg_head + 1) % h->m;
@@ -657,12 +765,12 @@ int aa_stats(aa_handle_t h, struct aa_stats* out, int flags) {
     p.op = OP_GRAM;
     p.gram = 2;
     p.c_in = h->mi;
-    for (int j = 0; j < h->mi; ++j) p.in[j] = qcol(h, j);
-    p.nin = h->mi;
+    Inputs in;
+    in.block(0, 0, h->mi);
     const int words = h->mi * (h->mi + 1) / 2;
     p.words = words;
     p.red_slot = NSLOT - 1;
-    RET_IF(launch_op<OP_GRAM>(h, p, 1));
+    RET_IF(launch_op<OP_GRAM>(h, p, in, 1));
     double* gbuf = h->red + (size_t)(NSLOT - 1) * LRED;
     if (h->nranks > 1) {
       ncclResult_t r = nccl().AllReduce(gbuf, gbuf, words, kNcclFloat64, kNcclSum, h->comm, h->stream);
