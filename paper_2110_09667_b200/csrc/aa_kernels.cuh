@@ -283,10 +283,57 @@ __device__ __forceinline__ int gram_block_I(int blk) {
   return I;
 }
 
+
+// Sum the per-warp DMMA Gram accumulators over the 8 warps through shared memory (the
+// stage ring is idle after the tile loop), in chunks of blocks, and write this CTA's
+// partial words.  mode 0: strict lower, rows < kg-1 -> off_gram, row kg-1 -> off_x (ICWY
+// after QRDelete + Alg. 4 l.1); 1: strict lower packed (stand-alone delete); 2: lower incl.
+// diagonal packed (loss of orthogonality).
+template <int NB8>
+__device__ void gram_epilogue(const KParams& p, const double* gc0, const double* gc1, double* buf,
+                              double* mypart, int kg, int mode, int off_x, int off_gram) {
+  constexpr int GB = NB8 * (NB8 + 1) / 2;
+  constexpr int CH = 8;  // blocks per chunk: 8 warps x 8 blocks x 64 doubles = 32 KB
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b0 = 0; b0 < GB; b0 += CH) {
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < GB; ++g)
+      if (g >= b0 && g < b0 + CH) {
+        buf[((warp * CH) + (g - b0)) * 64 + 2 * lane] = gc0[g];
+        buf[((warp * CH) + (g - b0)) * 64 + 2 * lane + 1] = gc1[g];
+      }
+    __syncthreads();
+    const int nb = min(CH, GB - b0);
+    for (int e = tid; e < nb * 64; e += NT) {
+      const int gl = e / 64, w = e % 64;
+      double s = 0.0;
+      for (int ww = 0; ww < NWARP; ++ww) s += buf[(ww * CH + gl) * 64 + w];
+      const int g = b0 + gl;
+      const int I = gram_block_I(g), J = g - I * (I + 1) / 2;
+      const int ln = w >> 1, ee = w & 1;
+      const int i = 8 * I + (ln >> 2), j = 8 * J + 2 * (ln & 3) + ee;
+      if (i >= kg) continue;
+      if (mode == 2) {
+        if (j <= i) mypart[i * (i + 1) / 2 + j] = s;
+      } else if (j < i) {
+        int wd;
+        if (mode == 1) wd = i * (i - 1) / 2 + j;
+        else if (i == kg - 1) wd = off_x + j;
+        else wd = off_gram + i * (i - 1) / 2 + j;
+        mypart[wd] = s;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------- kernel
-// OP: the op; NCW: phase-B columns per warp (0 = no block multi-dot); GRAM: DMMA Gram.
-template <int OP, int NCW, bool GRAM>
+// OP: the op; NCW: phase-B columns per warp (0 = no block multi-dot); NB8: 8-column
+// groups of the DMMA Gram (0 = no Gram).
+template <int OP, int NCW, int NB8>
 __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant__ KParams p) {
+  constexpr bool GRAM = NB8 > 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + head_bytes());
@@ -335,25 +382,23 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   }
 #pragma unroll
   for (int b = 0; b < NRB; ++b) roff[b] = (NCW > 0 && b < H.nr) ? H.rcol[b] * TR : 0;
-  // Gram accumulators (fp64 DMMA 8x8 blocks): up to 5 blocks per warp
-  constexpr int GB = GRAM ? 5 : 1;
+  // Gram accumulators (fp64 DMMA 8x8 blocks): every warp holds ALL NB8*(NB8+1)/2 lower
+  // blocks for its own k-steps (rows r0 = 4*(warp + 8*i) of each tile), so a k-step issues
+  // GB independent DMMAs sharing NB8 fragment loads; warps are summed at the end.
+  constexpr int GB = GRAM ? NB8 * (NB8 + 1) / 2 : 1;
   double gc0[GB], gc1[GB];
-  int gofa[GB], gofb[GB];
   const bool del_only = p.flags & F_DELETE_ONLY;
   const int kg = (OP == OP_GRAM) ? p.c_in : (del_only ? p.c_in - 1 : k);
-  const int nb8 = (kg + 7) / 8;
-  const int nblk8 = nb8 * (nb8 + 1) / 2;
   const bool do_gram = GRAM && p.gram != 0 && (OP == OP_GRAM ? kg >= 1 : kg >= 2);
+  int gfrag[NB8 > 0 ? NB8 : 1];
   {
     const int g_r = lane >> 2, g_c = lane & 3;
 #pragma unroll
-    for (int g = 0; g < GB; ++g) {
-      gc0[g] = gc1[g] = 0.0;
-      const int blk = warp + g * NWARP;
-      const int I = gram_block_I(blk), J = blk - I * (I + 1) / 2;
-      const int ca = 8 * I + g_r, cb = 8 * J + g_r;
-      gofa[g] = (ca < kg) ? ca * TR + g_c : -1;   // columns past kg contribute 0
-      gofb[g] = (cb < kg) ? cb * TR + g_c : -1;
+    for (int g = 0; g < GB; ++g) gc0[g] = gc1[g] = 0.0;
+#pragma unroll
+    for (int X = 0; X < (NB8 > 0 ? NB8 : 1); ++X) {
+      const int col = 8 * X + g_r;
+      gfrag[X] = (col < kg) ? col * TR + g_c : -1;   // columns past kg contribute 0
     }
   }
 
@@ -367,8 +412,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     mbar_wait(&bars[sidx], par);
 
     // ------------------------------------------------------------ phase A (row-wise)
-    const int r = tid;
-    if (r < TR) {
+    for (int r = tid; r < TR; r += NT) {
       const long long grow = row0 + r;
       if constexpr (OP == OP_K1) {
         const int ncols = del_only ? p.c_in : (p.recycle ? p.c_in : k);
@@ -536,16 +580,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       }
       if constexpr (GRAM) {
         if (do_gram) {
-          for (int r0 = 0; r0 < TR; r0 += 4) {
+          for (int r0 = 4 * warp; r0 < TR; r0 += 4 * NWARP) {
             const double* Sr = S + r0;
+            double fr[NB8];
 #pragma unroll
-            for (int g = 0; g < GB; ++g) {
-              if (warp + g * NWARP < nblk8) {
-                const double av = gofa[g] >= 0 ? Sr[gofa[g]] : 0.0;
-                const double bv = gofb[g] >= 0 ? Sr[gofb[g]] : 0.0;
-                dmma_8x8x4(gc0[g], gc1[g], av, bv);
-              }
-            }
+            for (int X = 0; X < NB8; ++X) fr[X] = gfrag[X] >= 0 ? Sr[gfrag[X]] : 0.0;
+#pragma unroll
+            for (int I = 0; I < NB8; ++I)
+#pragma unroll
+              for (int J = 0; J <= I; ++J) dmma_8x8x4(gc0[I * (I + 1) / 2 + J], gc1[I * (I + 1) / 2 + J], fr[I], fr[J]);
           }
         }
       }
@@ -590,27 +633,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       }
       if (tid == 0) mypart[2] = (blockIdx.x == 0 && !(p.flags & F_EXT_DF)) ? p.st->dx2_local : 0.0;
     }
-    if (do_gram) {
-      const int g_r = lane >> 2, g_c = lane & 3;
-#pragma unroll
-      for (int g = 0; g < GB; ++g) {
-        const int blk = warp + g * NWARP;
-        if (blk < nblk8) {
-          const int I = gram_block_I(blk), J = blk - I * (I + 1) / 2;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = 8 * I + g_r, j = 8 * J + 2 * g_c + e;
-            const double v = e ? gc1[g] : gc0[g];
-            if (j < i && i < kg) {
-              int w;
-              if (del_only) w = i * (i - 1) / 2 + j;
-              else if (i == kg - 1) w = L.off_x + j;
-              else w = L.off_gram + i * (i - 1) / 2 + j;
-              mypart[w] = v;
-            }
-          }
-        }
-      }
+    if constexpr (GRAM) {
+      if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, del_only ? 1 : 0, L.off_x, L.off_gram);
     }
   } else if constexpr (OP == OP_K2A_CGS2) {
 #pragma unroll
@@ -622,21 +646,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       }
     }
   } else if constexpr (OP == OP_GRAM) {
-    if (do_gram) {
-      const int g_r = lane >> 2, g_c = lane & 3;
-#pragma unroll
-      for (int g = 0; g < GB; ++g) {
-        const int blk = warp + g * NWARP;
-        if (blk < nblk8) {
-          const int I = gram_block_I(blk), J = blk - I * (I + 1) / 2;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = 8 * I + g_r, j = 8 * J + 2 * g_c + e;
-            const double v = e ? gc1[g] : gc0[g];
-            if (j <= i && i < kg) mypart[i * (i + 1) / 2 + j] = v;
-          }
-        }
-      }
+    if constexpr (GRAM) {
+      if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, 2, 0, 0);
     }
   } else {
     // row-wise accumulators: block reduction

@@ -117,21 +117,24 @@ double* dgcol(aa_ctx* c, int slot) { return c->DG + (size_t)slot * c->ld; }
 // shared memory (tools/stream_bench.cu: ~7 TB/s at 252-256 rows, 3-4 stages, 1 CTA/SM).
 // Kernels with a DMMA Gram take TR in {252,124,60,28} (bank skew), the others
 // TR in {256,128,64,32} (every 2-D box lands 128-byte aligned).
-void choose_tile(int nin, bool skew, int* tr, int* stages) {
+void choose_tile(int nin, bool skew, bool vec_only, int* tr, int* stages) {
   const size_t budget = 200 * 1024;
   const int trs_s[4] = {252, 124, 60, 28};
   const int trs_p[4] = {256, 128, 64, 32};
-  const int* trs = skew ? trs_s : trs_p;
-  for (int t = 0; t < 4; ++t) {
+  const int trs_v[6] = {1024, 512, 256, 128, 64, 32};   // vectors only: 1-D copies up to 8 KB
+  const int* trs = skew ? trs_s : (vec_only ? trs_v : trs_p);
+  const int nt = vec_only ? 6 : 4;
+  for (int t = 0; t < nt; ++t) {
     const size_t sb = align_up((size_t)nin * trs[t], 16) * sizeof(double);
     int s = (int)std::min<size_t>(MAXSTAGES, budget / sb);
+    if (vec_only && s > 2 && sb * s > budget / 2) s = std::max(3, (int)(budget / 2 / sb));  // leave room for 2 CTAs/SM
     if (s >= 3) {
       *tr = trs[t];
       *stages = s;
       return;
     }
   }
-  *tr = trs[3];
+  *tr = trs[nt - 1];
   *stages = 2;
 }
 
@@ -215,7 +218,7 @@ struct EvScope {
   }
 };
 
-template <int OP, int NCW, bool G>
+template <int OP, int NCW, int G>
 int launch_inst(aa_ctx* c, KParams& p, size_t smem, int cls) {
   static size_t attr_set = 0;
   if (smem > attr_set) {
@@ -238,8 +241,8 @@ int launch_inst(aa_ctx* c, KParams& p, size_t smem, int cls) {
   return AA_OK;
 }
 
-#define AA_NCW_CASES(OP, G)                         \
-  switch (ncw) {                                    \
+#define AA_NCW_CASES(OP, G)                                \
+  switch (ncw) {                                           \
     case 1: return launch_inst<OP, 1, G>(c, p, smem, cls); \
     case 2: return launch_inst<OP, 2, G>(c, p, smem, cls); \
     case 3: return launch_inst<OP, 3, G>(c, p, smem, cls); \
@@ -250,13 +253,18 @@ int launch_inst(aa_ctx* c, KParams& p, size_t smem, int cls) {
     case 8: return launch_inst<OP, 8, G>(c, p, smem, cls); \
     default: return launch_inst<OP, 9, G>(c, p, smem, cls); \
   }
+// K1 with the DMMA Gram: NB8 = ceil(k/8) and NCW = ceil((k+2)/8) in {NB8, NB8+1}
+#define AA_K1_GRAM_CASE(NB)                                                        \
+  case NB:                                                                         \
+    if (ncw == NB) return launch_inst<OP_K1, NB, NB>(c, p, smem, cls);             \
+    return launch_inst<OP_K1, (NB < 9 ? NB + 1 : 9), NB>(c, p, smem, cls);
 
 template <int OP>
 int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   const bool gram = (OP == OP_GRAM) || (OP == OP_K1 && p.gram != 0);
   const int nin = in.ncols() + in.nvec;
   int tr, stages;
-  choose_tile(std::max(nin, 1), gram, &tr, &stages);
+  choose_tile(std::max(nin, 1), gram, in.nblk == 0 && nin > 0, &tr, &stages);
   p.tr = tr;
   p.stages = stages;
   p.nin = nin;
@@ -284,17 +292,51 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   if constexpr (OP == OP_K1) {
     const int ncw = (p.flags & F_DELETE_ONLY) ? 1 : (p.k + 2 + NWARP - 1) / NWARP;
     if (gram) {
-      AA_NCW_CASES(OP_K1, true)
+      const int kg = (p.flags & F_DELETE_ONLY) ? p.c_in - 1 : p.k;
+      const int nb8 = (kg + 7) / 8;
+      if (p.flags & F_DELETE_ONLY) {
+        switch (nb8) {
+          case 1: return launch_inst<OP_K1, 1, 1>(c, p, smem, cls);
+          case 2: return launch_inst<OP_K1, 1, 2>(c, p, smem, cls);
+          case 3: return launch_inst<OP_K1, 1, 3>(c, p, smem, cls);
+          case 4: return launch_inst<OP_K1, 1, 4>(c, p, smem, cls);
+          case 5: return launch_inst<OP_K1, 1, 5>(c, p, smem, cls);
+          case 6: return launch_inst<OP_K1, 1, 6>(c, p, smem, cls);
+          case 7: return launch_inst<OP_K1, 1, 7>(c, p, smem, cls);
+          default: return launch_inst<OP_K1, 1, 8>(c, p, smem, cls);
+        }
+      }
+      switch (nb8) {
+        AA_K1_GRAM_CASE(1)
+        AA_K1_GRAM_CASE(2)
+        AA_K1_GRAM_CASE(3)
+        AA_K1_GRAM_CASE(4)
+        AA_K1_GRAM_CASE(5)
+        AA_K1_GRAM_CASE(6)
+        AA_K1_GRAM_CASE(7)
+        default:
+          if (ncw == 8) return launch_inst<OP_K1, 8, 8>(c, p, smem, cls);
+          return launch_inst<OP_K1, 9, 8>(c, p, smem, cls);
+      }
     } else {
-      AA_NCW_CASES(OP_K1, false)
+      AA_NCW_CASES(OP_K1, 0)
     }
   } else if constexpr (OP == OP_K2A_CGS2) {
     const int ncw = std::max(1, (p.k + NWARP - 1) / NWARP);
-    AA_NCW_CASES(OP_K2A_CGS2, false)
+    AA_NCW_CASES(OP_K2A_CGS2, 0)
   } else if constexpr (OP == OP_GRAM) {
-    return launch_inst<OP_GRAM, 0, true>(c, p, smem, cls);
+    switch ((p.c_in + 7) / 8) {
+      case 1: return launch_inst<OP_GRAM, 0, 1>(c, p, smem, cls);
+      case 2: return launch_inst<OP_GRAM, 0, 2>(c, p, smem, cls);
+      case 3: return launch_inst<OP_GRAM, 0, 3>(c, p, smem, cls);
+      case 4: return launch_inst<OP_GRAM, 0, 4>(c, p, smem, cls);
+      case 5: return launch_inst<OP_GRAM, 0, 5>(c, p, smem, cls);
+      case 6: return launch_inst<OP_GRAM, 0, 6>(c, p, smem, cls);
+      case 7: return launch_inst<OP_GRAM, 0, 7>(c, p, smem, cls);
+      default: return launch_inst<OP_GRAM, 0, 8>(c, p, smem, cls);
+    }
   } else {
-    return launch_inst<OP, 0, false>(c, p, smem, cls);
+    return launch_inst<OP, 0, 0>(c, p, smem, cls);
   }
 }
 
