@@ -230,11 +230,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2110_09667_b200 import aa
 
-    uid = None
+    uid, comm = None, None
     if world > 1:
-        obj = [aa.aa_comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        dist.barrier()
+        comm = aa.torch_nccl_comm()   # libaa borrows the process group's NCCL communicator
 
     n_local = int(args.n_local)
     offset = rank * n_local
@@ -261,7 +260,7 @@ def main():
 
     def measure(variant, m, steps, warmup, with_clocks=False, e2e=False):
         s = aa.AndersonSolver(n_local, m, variant, rank=rank, nranks=world, unique_id=uid,
-                              stream=stream, profile=1, n_global=n_local * world,
+                              nccl_comm=comm, stream=stream, profile=1, n_global=n_local * world,
                               icwy_merged=args.icwy_merged)
         x = torch.zeros(n_local, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)

@@ -121,6 +121,13 @@ int aa_comm_unique_id(void* id128);
  * Collective over the ranks when nranks > 1. */
 int aa_create(aa_handle_t* h, int64_t n_local, int m, int qr_variant, int rank, int nranks,
               const void* id128, void* cuda_stream);
+/* Same as aa_create with nranks > 1, but BORROWS an already-initialised NCCL
+ * communicator (ncclComm_t of nranks ranks, this process = rank), e.g. the one a
+ * torch.distributed NCCL process group owns.  libaa never frees it; the caller must
+ * not destroy it before aa_destroy and must not run other collectives on it
+ * concurrently with libaa calls. */
+int aa_create_with_comm(aa_handle_t* h, int64_t n_local, int m, int qr_variant, int rank, int nranks,
+                        void* nccl_comm, void* cuda_stream);
 int aa_set_option(aa_handle_t h, int opt, double val);
 
 /* Alg. 1 l.1: f_0 = G(x_0) - x_0, remember G(x_0) and f_0, x1_out = G(x_0).

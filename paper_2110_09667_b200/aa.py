@@ -23,7 +23,7 @@ AA_OK, AA_ERR_BREAKDOWN = 0, 6
 PHASES = ("qradd", "qrdelete", "lsp_rhs", "norm_check", "other")
 
 # every symbol include/aa.h and include/aa_testing.h declare
-EXPORTS = ("aa_comm_unique_id", "aa_create", "aa_set_option", "aa_init", "aa_step", "aa_step_host",
+EXPORTS = ("aa_comm_unique_id", "aa_create", "aa_create_with_comm", "aa_set_option", "aa_init", "aa_step", "aa_step_host",
            "aa_delete_oldest", "aa_stats", "aa_reset", "aa_destroy", "aa_status_string",
            "aa_test_qradd", "aa_get_small", "aa_get_q", "aa_timings", "aa_kernel_launches",
            "aa_fill_uniform", "aa_build_info")
@@ -45,6 +45,7 @@ def _load():
     sig = {
         "aa_comm_unique_id": (i32, [vp]),
         "aa_create": (i32, [C.POINTER(vp), i64, i32, i32, i32, i32, vp, vp]),
+        "aa_create_with_comm": (i32, [C.POINTER(vp), i64, i32, i32, i32, i32, vp, vp]),
         "aa_set_option": (i32, [vp, i32, dbl]),
         "aa_init": (i32, [vp, vp, vp, vp]),
         "aa_step": (i32, [vp, vp, vp, vp]),
@@ -125,6 +126,24 @@ def aa_create(n_local: int, m: int, qr_variant, rank: int = 0, nranks: int = 1,
     uid = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
     _chk(_lib.aa_create(C.byref(h), n_local, m, v, rank, nranks, uid, _stream_ptr(stream)), "aa_create")
     return h.value
+
+
+def aa_create_with_comm(n_local: int, m: int, qr_variant, rank: int, nranks: int, nccl_comm: int,
+                        stream=None) -> int:
+    v = VARIANT_IDS[qr_variant] if isinstance(qr_variant, str) else int(qr_variant)
+    h = C.c_void_p()
+    _chk(_lib.aa_create_with_comm(C.byref(h), n_local, m, v, rank, nranks, nccl_comm, _stream_ptr(stream)),
+         "aa_create_with_comm")
+    return h.value
+
+
+def torch_nccl_comm(group=None) -> int:
+    """ncclComm_t of a torch.distributed NCCL process group on the current device (the
+    group must be initialised eagerly, e.g. init_process_group(..., device_id=...))."""
+    import torch
+    import torch.distributed as dist
+    pg = group or dist.distributed_c10d._get_default_group()
+    return pg._get_backend(torch.device("cuda", torch.cuda.current_device()))._comm_ptr()
 
 
 def aa_set_option(h: int, opt: int, val: float) -> None:
@@ -228,9 +247,12 @@ class AndersonSolver:
     """Owns one libaa handle.  Marshalling only (no arithmetic happens here)."""
 
     def __init__(self, n_local, m, variant="dcgs2", rank=0, nranks=1, unique_id=None, stream=None,
-                 **options):
+                 nccl_comm=None, **options):
         self.n_local, self.m = n_local, m
-        self.h = aa_create(n_local, m, variant, rank, nranks, unique_id, stream)
+        if nranks > 1 and nccl_comm is not None:
+            self.h = aa_create_with_comm(n_local, m, variant, rank, nranks, nccl_comm, stream)
+        else:
+            self.h = aa_create(n_local, m, variant, rank, nranks, unique_id, stream)
         names = {"beta": OPT_DAMPING_BETA, "icwy_merged": OPT_ICWY_DELETE, "dcgs2_cond": OPT_DCGS2_COND,
                  "dcgs2_rscale": OPT_DCGS2_RSCALE, "breakdown_eps": OPT_BREAKDOWN_EPS,
                  "profile": OPT_PROFILE, "n_global": OPT_N_GLOBAL}

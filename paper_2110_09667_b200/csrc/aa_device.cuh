@@ -76,6 +76,7 @@ constexpr int NBLK_MAX = 3;   // 2-D column blocks (tensor maps) per kernel
 struct alignas(64) KParams {
   CUtensorMap tm[NBLK_MAX];   // 2-D maps over Q or the Delta G ring (rows x m columns)
   int blk_gcol[NBLK_MAX];     // first global column of each block
+  int blk_which[NBLK_MAX];    // host bookkeeping: 0 = Q, 1 = Delta G ring
   int blk_ncols[NBLK_MAX];
   int nblk, nvec;
   const double* vec[NVEC_MAX];

@@ -26,7 +26,7 @@
 
 namespace aa {
 
-constexpr int MAXSTAGES = 4;
+constexpr int MAXSTAGES = 8;
 
 struct HeadArea {
   double coef[NIN_MAX];
@@ -34,6 +34,7 @@ struct HeadArea {
   double sc[NIN_MAX];
   double cs[MMAX];
   double sn[MMAX];
+  double2 rot[2 * MMAX];   // K1: {c_j, s_j*sc_{j+1}}, {-s_j, c_j*sc_{j+1}} (scale folded in)
   double scal[8];
   double redw[NWARP][4];
   int lcol[MMAX + 2];
@@ -177,6 +178,13 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
   if constexpr (OP == OP_K1) {
     if (p.recycle) k3_givens_delete(p.st->R, p.c_in, scratch, H.cs, H.sn);
     for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->scale[j];
+    __syncwarp();
+    if (p.recycle)
+      for (int j = lane; j < p.c_in - 1; j += 32) {
+        const double c = H.cs[j], s = H.sn[j], scn = H.sc[j + 1];
+        H.rot[2 * j] = make_double2(c, s * scn);
+        H.rot[2 * j + 1] = make_double2(-s, c * scn);
+      }
     if (lane == 0) {
       if (p.flags & F_DELETE_ONLY) {
         H.na = 0;
@@ -439,14 +447,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
             // QRDelete on Q: streaming carry form of the m-1 Givens rotations of adjacent
             // column pairs; the last carry is the dropped column.
             double carry = S[r] * H.sc[0];
+            double* Qg = p.Q + grow;
 #pragma unroll 4
             for (int j = 0; j < p.c_in - 1; ++j) {
-              const double qn = S[(size_t)(j + 1) * TR + r] * H.sc[j + 1];
-              const double c = H.cs[j], s = H.sn[j];
-              const double out = fma(c, carry, s * qn);
-              carry = fma(-s, carry, c * qn);
+              const double qn = S[(size_t)(j + 1) * TR + r];   // stored (lazily scaled) column
+              const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
+              const double out = fma(a.x, carry, a.y * qn);   // c*carry + s*sc*q
+              carry = fma(b.x, carry, b.y * qn);               // -s*carry + c*sc*q
               S[(size_t)j * TR + r] = out;
-              p.Q[(size_t)j * p.ld + grow] = out;
+              Qg[(size_t)j * p.ld] = out;
             }
           } else {
             for (int j = 0; j < ncols; ++j) S[(size_t)j * TR + r] *= H.sc[j];

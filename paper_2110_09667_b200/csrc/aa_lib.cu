@@ -9,6 +9,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -72,6 +73,7 @@ struct aa_ctx {
   double *red = nullptr, *part = nullptr;
   double *hx = nullptr, *hg = nullptr, *hxn = nullptr;  // staging for aa_step_host
   ncclComm_t comm = nullptr;
+  bool own_comm = false;
   // window bookkeeping (host; depends only on i, m_i)
   int64_t iter = 0;
   int mi = 0, dg_head = 0;
@@ -117,25 +119,32 @@ double* dgcol(aa_ctx* c, int slot) { return c->DG + (size_t)slot * c->ld; }
 // shared memory (tools/stream_bench.cu: ~7 TB/s at 252-256 rows, 3-4 stages, 1 CTA/SM).
 // Kernels with a DMMA Gram take TR in {252,124,60,28} (bank skew), the others
 // TR in {256,128,64,32} (every 2-D box lands 128-byte aligned).
-void choose_tile(int nin, bool skew, bool vec_only, int* tr, int* stages) {
-  const size_t budget = 200 * 1024;
-  const int trs_s[4] = {252, 124, 60, 28};
-  const int trs_p[4] = {256, 128, 64, 32};
-  const int trs_v[6] = {1024, 512, 256, 128, 64, 32};   // vectors only: 1-D copies up to 8 KB
+// Tile rows TR and stage count NS of one launch.  Two CTAs per SM with a 2-stage ring
+// each when registers allow (<= 128 per thread): the largest TR <= max_tr whose two stages
+// fit in ~104 KB.  Otherwise one CTA with >= 3 stages in ~200 KB.  Kernels with a DMMA
+// Gram take TR in {252,124,60,28} (bank skew), vector-only kernels up to 1024 rows
+// (1-D copies of 8 KB), the rest TR in {256,128,64,32} (2-D boxes 128-byte aligned).
+// Measured on B200 (tools/tune_tiles.sh, config 2, m = 20): see DESIGN.md §7.
+bool choose_tile(int nin, bool skew, bool vec_only, size_t budget, int min_stages, int max_stages, int max_tr,
+                 int* tr, int* stages) {
+  static const int trs_s[] = {252, 124, 60, 28};
+  static const int trs_p[] = {256, 128, 64, 32};
+  static const int trs_v[] = {1024, 512, 256, 128, 64, 32};
   const int* trs = skew ? trs_s : (vec_only ? trs_v : trs_p);
   const int nt = vec_only ? 6 : 4;
   for (int t = 0; t < nt; ++t) {
+    if (trs[t] > max_tr) continue;
     const size_t sb = align_up((size_t)nin * trs[t], 16) * sizeof(double);
-    int s = (int)std::min<size_t>(MAXSTAGES, budget / sb);
-    if (vec_only && s > 2 && sb * s > budget / 2) s = std::max(3, (int)(budget / 2 / sb));  // leave room for 2 CTAs/SM
-    if (s >= 3) {
+    const int s = (int)std::min<size_t>((size_t)max_stages, budget / sb);
+    if (s >= min_stages) {
       *tr = trs[t];
       *stages = s;
-      return;
+      return true;
     }
   }
   *tr = trs[nt - 1];
   *stages = 2;
+  return false;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -218,13 +227,71 @@ struct EvScope {
   }
 };
 
+// Launch one instantiation.  The tile (TR rows x stages) is chosen here, knowing the
+// kernel's register count: when registers allow two 256-thread CTAs per SM (<= 128 per
+// thread) the stage ring is sized for ~110 KB per CTA so two CTAs share each SM (twice
+// the warps to hide the fp64 / shared-memory latencies of phases A and B); otherwise one
+// CTA gets ~200 KB.
 template <int OP, int NCW, int G>
-int launch_inst(aa_ctx* c, KParams& p, size_t smem, int cls) {
+int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
+  static int regs = -1;
+  if (regs < 0) {
+    cudaFuncAttributes fa;
+    CUDA_TRY(c, cudaFuncGetAttributes(&fa, aa_stream_kernel<OP, NCW, G>));
+    regs = fa.numRegs;
+  }
+  const bool skew = (G > 0);
+  const bool vec_only = (p.nblk == 0 && p.nin > 0);
+  const int nin = std::max(p.nin, 1);
+  int tr = 0, stages = 0;
+  bool ok = false;
+  if (regs <= 128) {
+    if (OP == OP_K1 && !skew)  // K1 without a Gram: largest tile that still gets 4 stages
+      ok = choose_tile(nin, skew, vec_only, 104 * 1024, 4, 4, 256, &tr, &stages);
+    if (!ok) {
+      // 2 stages of the largest tile; more stages only when the tile is small (few columns)
+      ok = choose_tile(nin, skew, vec_only, 104 * 1024, 2, MAXSTAGES, vec_only ? 1024 : 256, &tr, &stages);
+      if (ok && !vec_only) {
+        const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
+        stages = (int)std::max<size_t>(2, std::min<size_t>(MAXSTAGES, (96 * 1024 + sb - 1) / sb));
+        if ((size_t)stages * sb > 104 * 1024) stages = (int)((104 * 1024) / sb);
+      } else if (ok) {
+        stages = 2;
+      }
+    }
+  }
+  if (!ok) choose_tile(nin, skew, vec_only, 200 * 1024, 2, 3, 1024, &tr, &stages);
+  // tuning override (tools only): AA_TILE="<op>:<tr>:<stages>[,<op>:<tr>:<stages>...]"
+  if (const char* ov = getenv("AA_TILE")) {
+    const char* q = ov;
+    while (*q) {
+      int o, t, s, used = 0;
+      if (sscanf(q, "%d:%d:%d%n", &o, &t, &s, &used) == 3 && used > 0) {
+        if (o == OP && t >= 4 && s >= 1 && s <= MAXSTAGES) {
+          tr = skew ? (t / 4) * 4 : t;
+          stages = s;
+        }
+        q += used;
+        if (*q == ',') ++q;
+      } else {
+        break;
+      }
+    }
+  }
+  p.tr = tr;
+  p.stages = stages;
+  for (int b = 0; b < p.nblk; ++b) {
+    const CUtensorMap* m = get_map(c, p.blk_which[b], p.blk_ncols[b], tr);
+    if (!m) return fail(c, AA_ERR_CUDA);
+    p.tm[b] = *m;
+  }
+  const size_t stage_bytes = (size_t)stages * align_up((size_t)nin * tr, 16) * sizeof(double);
+  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scratch_bytes());
   static size_t attr_set = 0;
   if (smem > attr_set) {
     CUDA_TRY(c, cudaFuncSetAttribute(aa_stream_kernel<OP, NCW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    attr_set = smem;
+                                     (int)std::max<size_t>(smem, 110 * 1024)));
+    attr_set = std::max<size_t>(smem, 110 * 1024);
   }
   int per_sm = 1;
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP, NCW, G>, NT, smem));
@@ -262,26 +329,20 @@ int launch_inst(aa_ctx* c, KParams& p, size_t smem, int cls) {
 template <int OP>
 int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   const bool gram = (OP == OP_GRAM) || (OP == OP_K1 && p.gram != 0);
+  (void)gram;
   const int nin = in.ncols() + in.nvec;
-  int tr, stages;
-  choose_tile(std::max(nin, 1), gram, in.nblk == 0 && nin > 0, &tr, &stages);
-  p.tr = tr;
-  p.stages = stages;
   p.nin = nin;
   p.vb = in.ncols();
   p.nblk = in.nblk;
   p.nvec = in.nvec;
   p.exact_vec = in.exact;
   for (int b = 0; b < in.nblk; ++b) {
-    const CUtensorMap* m = get_map(c, in.blk_which[b], in.blk_ncols[b], tr);
-    if (!m) return fail(c, AA_ERR_CUDA);
-    p.tm[b] = *m;
+    p.blk_which[b] = in.blk_which[b];
     p.blk_gcol[b] = in.blk_gcol[b];
     p.blk_ncols[b] = in.blk_ncols[b];
   }
   for (int i = 0; i < in.nvec; ++i) p.vec[i] = in.vec[i];
-  const size_t stage_bytes = (size_t)stages * align_up((size_t)std::max(nin, 1) * tr, 16) * sizeof(double);
-  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scratch_bytes());
+  const size_t smem = 0;
   p.st = c->st;
   p.red = c->red;
   p.part = c->part;
@@ -564,10 +625,10 @@ int aa_comm_unique_id(void* id128) {
   return AA_OK;
 }
 
-int aa_create(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank, int nranks,
-              const void* id128, void* cuda_stream) {
+static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank, int nranks,
+                       const void* id128, void* borrowed_comm, void* cuda_stream) {
   if (!out || n_local < 1 || m < 1 || m > MMAX || qr_variant < 0 || qr_variant > 3 || nranks < 1 ||
-      rank < 0 || rank >= nranks || (nranks > 1 && !id128))
+      rank < 0 || rank >= nranks || (nranks > 1 && !id128 && !borrowed_comm))
     return AA_ERR_ARG;
   *out = nullptr;
   aa_ctx* c = new aa_ctx();
@@ -603,14 +664,42 @@ int aa_create(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank
       cudaMemset(c->red, 0, sizeof(double) * LRED * NSLOT) != cudaSuccess ||
       cudaMemset(c->st, 0, sizeof(SmallState)) != cudaSuccess)
     return bail(AA_ERR_CUDA);
-  if (nranks > 1) {
-    if (!nccl().ok) return bail(AA_ERR_NCCL);
+  if (nranks > 1 && borrowed_comm) {
+    if (!nccl().ok) {
+      fprintf(stderr, "libaa: libnccl.so.2 could not be loaded (dlopen)\n");
+      return bail(AA_ERR_NCCL);
+    }
+    c->comm = (ncclComm_t)borrowed_comm;
+    c->own_comm = false;
+  } else if (nranks > 1) {
+    if (!nccl().ok) {
+      fprintf(stderr, "libaa: libnccl.so.2 could not be loaded (dlopen)\n");
+      return bail(AA_ERR_NCCL);
+    }
     ncclUniqueId id;
     memcpy(&id, id128, sizeof(id));
-    if (nccl().CommInitRank(&c->comm, nranks, id, rank) != 0) return bail(AA_ERR_NCCL);
+    const ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, id, rank);
+    if (r != 0) {
+      fprintf(stderr, "libaa: ncclCommInitRank(rank %d of %d) failed: %d %s\n", rank, nranks, (int)r,
+              nccl().GetErrorString ? nccl().GetErrorString(r) : "");
+      c->comm = nullptr;
+      return bail(AA_ERR_NCCL);
+    }
+    c->own_comm = true;
   }
   *out = c;
   return AA_OK;
+}
+
+int aa_create(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank, int nranks,
+              const void* id128, void* cuda_stream) {
+  return create_impl(out, n_local, m, qr_variant, rank, nranks, id128, nullptr, cuda_stream);
+}
+
+int aa_create_with_comm(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank, int nranks,
+                        void* nccl_comm, void* cuda_stream) {
+  if (nranks > 1 && !nccl_comm) return AA_ERR_ARG;
+  return create_impl(out, n_local, m, qr_variant, rank, nranks, nullptr, nccl_comm, cuda_stream);
 }
 
 int aa_set_option(aa_handle_t h, int opt, double val) {
@@ -866,7 +955,7 @@ int aa_destroy(aa_handle_t h) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
-  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
   cudaFree(h->Q);
   cudaFree(h->DG);
   cudaFree(h->fp);
