@@ -69,6 +69,16 @@ class Reducer:
             tot = tot + A[lo:hi].T @ v[lo:hi]
         return tot
 
+    def matT_mat(self, A: np.ndarray, B: np.ndarray) -> np.ndarray:
+        """A^T B (several right-hand sides) as ONE fused reduction: the merged
+        "Delayed Sync" + "Sync" of Alg. 4 l.1-2 and Alg. 6 l.1/l.3."""
+        if self.p == 1:
+            return A.T @ B
+        tot = np.zeros((A.shape[1], B.shape[1]))
+        for lo, hi in self._bounds(A.shape[0]):
+            tot = tot + A[lo:hi].T @ B[lo:hi]
+        return tot
+
     def gram(self, A: np.ndarray) -> np.ndarray:
         if self.p == 1:
             return A.T @ A
@@ -166,9 +176,10 @@ def qradd_icwy(st: QRState, v: np.ndarray, led: Ledger, red: Reducer, vnorm0: fl
     if k >= 1:
         Qk = st.Q[:, :k]
         # l.1: T_{m_i-2, 0:m_i-2} <- Q_{:,0:m_i-2}^T Q_{:,m_i-2}      (Delayed Sync)
-        row = red.matT_vec(Qk, st.Q[:, k - 1])
-        # l.2: R_{0:m_i-2, m_i-1} <- Q_{:,0:m_i-2}^T Delta f          (Sync, merged with l.1)
-        rcol = red.matT_vec(Qk, v)
+        # l.2: R_{0:m_i-2, m_i-1} <- Q_{:,0:m_i-2}^T Delta f          (Sync)
+        # merged into one reduction: Q^T [q_{m_i-2}, Delta f]
+        both = red.matT_mat(Qk, np.stack([st.Q[:, k - 1], v], axis=1))
+        row, rcol = both[:, 0], both[:, 1]
         led.sync("qradd")
         st.T[k - 1, :k] = row
         st.T[k - 1, k - 1] = 1.0                          # l.3
@@ -207,9 +218,16 @@ def qradd_dcgs2(st: QRState, v: np.ndarray, led: Ledger, red: Reducer, vnorm0: f
     mi_new = k + 1
     if k >= 1:
         Qk = st.Q[:, :k]
-        rcol = red.matT_vec(Qk, v)                        # l.1 (Delayed Sync)
-        if mi_new > cond and k >= 2:                      # l.2 "if m_i > 3"
-            s = red.matT_vec(st.Q[:, :k - 1], st.Q[:, k - 1])   # l.3 (Sync, merged with l.1)
+        reortho = mi_new > cond and k >= 2                # l.2 "if m_i > 3"
+        # l.1 (Delayed Sync) and l.3 (Sync) in ONE reduction:
+        # Q_{0:m_i-2}^T [Delta f, q_{m_i-2}]; s is the first m_i-2 entries of column 2
+        if reortho:
+            both = red.matT_mat(Qk, np.stack([v, st.Q[:, k - 1]], axis=1))
+            rcol = both[:, 0]
+        else:
+            rcol = red.matT_vec(Qk, v)                    # l.1 alone
+        if reortho:
+            s = both[:k - 1, 1]                           # l.3: Q_{:,0:m_i-3}^T Q_{:,m_i-2}
             # l.4 read as Q_{:,m_i-2} <- Q_{:,m_i-2} - Q_{:,0:m_i-3} s  (reading A1)
             st.Q[:, k - 1] = st.Q[:, k - 1] - st.Q[:, :k - 1] @ s
             if rscale:
