@@ -209,6 +209,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--ref-n", type=float, default=1e6)
     ap.add_argument("--sweep", action="store_true", help="also sweep m in {5,10,20,50} x variants")
+    ap.add_argument("--sweep-n", action="store_true",
+                    help="latency regime: n_local in {1e3..1e7} x variants at --m (paper's GPU size 1.5e6, P:513)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--only-headline", action="store_true")
@@ -327,6 +329,40 @@ def main():
         torch.cuda.empty_cache()
         return res, clocks, e2e_res
 
+    def measure_n(variant, m, nl, steps, warmup):
+        """Recycle-step latency at n_local = nl (device events around aa_step, no per-kernel
+        profiling events).  Returns us/iter (max over ranks) and the allreduce count."""
+        dn = torch.empty(nl, dtype=torch.float64, device="cuda")
+        bn = torch.empty_like(dn)
+        aa.aa_fill_uniform(dn, nl, -0.9, 0.9, stream_id=1, offset=rank * nl, stream=stream)
+        aa.aa_fill_uniform(bn, nl, -1.0, 1.0, stream_id=2, offset=rank * nl, stream=stream)
+        Gn = lambda x: torch.addcmul(bn, dn, x)
+        s = aa.AndersonSolver(nl, m, variant, rank=rank, nranks=world, nccl_comm=comm, stream=stream,
+                              n_global=nl * world)
+        x = torch.zeros(nl, dtype=torch.float64, device="cuda")
+        xn = torch.empty_like(x)
+        s.init(x, Gn(x), xn)
+        x, xn = xn, x
+        for _ in range(m + warmup):
+            s.step(x, Gn(x), xn)
+            x, xn = xn, x
+        gs = [torch.empty_like(x) for _ in range(2)]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        barrier()
+        for i in range(steps):
+            g = Gn(x)
+            ev[i][0].record(stream)
+            s.step(x, g, xn)
+            ev[i][1].record(stream)
+            x, xn = xn, x
+        barrier()
+        t = sorted(a.elapsed_time(b_) for a, b_ in ev)
+        st = s.stats()
+        s.close()
+        return {"us_per_iter_median": max_over_ranks(t[len(t) // 2]) * 1e3,
+                "us_per_iter_min": max_over_ranks(t[0]) * 1e3, "allreduces": st.allreduce_last,
+                "sync_points": st.sync_points_last}
+
     V = 8 * n_local
     head, clocks, e2e = measure(args.variant, args.m, args.steps, args.warmup, with_clocks=True,
                                 e2e=not args.no_e2e)
@@ -351,6 +387,12 @@ def main():
                 sweep[f"{v}_m{m}"] = {"us_per_iter": r["ms_per_step"] * 1e3,
                                       "step_hbm_frac": step_bytes(v, m, V) / (r["ms_per_step"] * 1e-3) / (peak * 1e9),
                                       "k1_frac": k1_bytes(m, V) / (r["k1_ms"] * 1e-3) / (peak * 1e9)}
+
+    small_n = {}
+    if args.sweep_n:
+        for nl in (1000, 10000, 100000, 1500000, 10000000):
+            for v in VARIANTS:
+                small_n[f"{v}_n{nl}"] = measure_n(v, args.m, nl, 20, 5)
 
     k1b = k1_bytes(args.m, V)
     achieved = k1b / (head["k1_ms"] * 1e-3) / 1e9
@@ -379,6 +421,8 @@ def main():
                 "variants": variants}
         if sweep:
             line["sweep"] = sweep
+        if small_n:
+            line["small_n"] = small_n
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -35,13 +35,25 @@ enum Flags : int {
   F_COMMIT_ONLY = 4   // K4: no rows, only the small-factor commit
 };
 
-// Replicated small factors (identical on every rank: every rank recomputes them
-// from the same allreduce results).  Written only by the last CTA of a kernel.
-struct SmallState {
-  double R[MMAX * MMAX];     // column-major, leading dim MMAX
+// Replicated small factors (identical on every rank: every rank recomputes them from the
+// same allreduce results).  Double-buffered: every kernel of a step reads version `ver`;
+// CTA 0 of the step's last kernel (K4) writes version `ver ^ 1` straight from its head
+// (no other CTA reads it during that kernel), so nothing is recomputed at commit time.
+// Each version also carries the QRDelete of its own R precomputed (Givens coefficients
+// and the re-triangularised R), so the next recycle step's heads only load them.
+struct Factors {
+  double R[MMAX * MMAX];     // column-major, leading dim MMAX, K x K valid
   double T[MMAX * MMAX];     // ICWY: I + L (reading A5), column-major
+  double Rdel[MMAX * MMAX];  // R after QRDelete: (K-1) x (K-1)
   double scale[MMAX];        // lazy normalisation: Q_j(true) = scale[j] * Q_j(stored)
   double gamma[MMAX];
+  double cs[MMAX], sn[MMAX]; // Givens coefficients of QRDelete(R)
+  int K;                     // columns of R
+  int has_del;
+};
+
+struct SmallState {
+  Factors f[2];
   double dx2_local;          // this rank's ||x_{i+1} - x_i||^2 from the last update
   double f2;                 // ||f_i||^2 (global) of the last step
   double rratio_min;         // min R_kk / ||Delta f||
@@ -107,6 +119,7 @@ struct alignas(64) KParams {
   double* dg_out;   // Delta G ring slot written by K1
   double* x_out;    // K4 output
   SmallState* st;
+  int ver;          // factor version read by this step (written: ver ^ 1, by K4)
   double* red;      // reduction slots (slot s at red + s*LRED)
   double* part;     // per-CTA partials (CTA b at part + b*LRED)
 };
@@ -189,9 +202,13 @@ __device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double*
   __syncwarp();
   for (int j = 0; j < nc; ++j) {
     const double a = Rw[j + j * MMAX], b = Rw[j + 1 + j * MMAX];
-    const double rho = hypot(a, b);
-    const double c = rho > 0.0 ? a / rho : 1.0;
-    const double s = rho > 0.0 ? b / rho : 0.0;
+    // rho = hypot(a, b) >= 0; the plain form is exact to rounding unless a^2 + b^2 would
+    // over/underflow, where hypot's scaling takes over.  One reciprocal, two products.
+    const double aa = fabs(a), bb = fabs(b), mx = fmax(aa, bb);
+    const double rho = (mx < 1e150 && mx > 1e-150) ? sqrt(fma(a, a, b * b)) : hypot(a, b);
+    const double ri = rho > 0.0 ? 1.0 / rho : 0.0;
+    const double c = rho > 0.0 ? a * ri : 1.0;
+    const double s = rho > 0.0 ? b * ri : 0.0;
     for (int l = j + 1 + lane; l < nc; l += 32) {
       const double h1 = Rw[j + l * MMAX], h2 = Rw[j + 1 + l * MMAX];
       Rw[j + l * MMAX] = __dadd_rn(__dmul_rn(c, h1), __dmul_rn(s, h2));
@@ -223,9 +240,14 @@ __device__ void k3_forward_unit_lower(const double* T, double* r, int k) {
 // Back substitution R gamma = c (Alg. 2 l.9), R upper triangular K x K; c overwritten.
 __device__ void k3_back_subst(const double* R, double* c, double* gamma, int K) {
   const int lane = threadIdx.x & 31;
+  // reciprocals of the diagonal in parallel, so the serial chain has no division
+  double rinv0 = 0.0, rinv1 = 0.0;
+  if (lane < K) rinv0 = 1.0 / R[lane + lane * MMAX];
+  if (lane + 32 < K) rinv1 = 1.0 / R[(lane + 32) + (lane + 32) * MMAX];
   for (int j = K - 1; j >= 0; --j) {
     __syncwarp();
-    const double gj = c[j] / R[j + j * MMAX];
+    const double rj = __shfl_sync(0xffffffffu, j < 32 ? rinv0 : rinv1, j & 31);
+    const double gj = c[j] * rj;
     if (lane == 0) gamma[j] = gj;
     for (int i = lane; i < j; i += 32) c[i] -= R[i + j * MMAX] * gj;
   }

@@ -51,7 +51,7 @@ __host__ __device__ constexpr size_t scratch_bytes() { return (2 * MMAX * MMAX +
 __device__ __forceinline__ double cur_scale(const KParams& p, int j) {
   // scale of stored Q column j as seen after this step's K1: rotated columns (QRDelete)
   // were written as true values.
-  return p.recycle ? 1.0 : p.st->scale[j];
+  return p.recycle ? 1.0 : p.st->f[p.ver].scale[j];
 }
 
 // ---------------------------------------------------------------------------- heads
@@ -68,7 +68,7 @@ __device__ void icwy_assemble_T(const KParams& p, const double* red0, double* Tw
     else if (p.flags & F_DELETE_ONLY) v = red0[i * (i - 1) / 2 + j];
     else if (i == k - 1) v = red0[L.off_x + j];
     else if (p.recycle) v = red0[L.off_gram + i * (i - 1) / 2 + j];
-    else v = p.st->T[i + j * MMAX];
+    else v = p.st->f[p.ver].T[i + j * MMAX];
     Tw[i + j * MMAX] = v;
   }
   __syncwarp();
@@ -92,16 +92,14 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   const double* red0 = p.red;
   const int k = p.k;
   K4Head out{};
-  const int mold = k + 1;
-  if (p.recycle) {
-    k3_givens_delete(p.st->R, mold, Rw, H.cs, H.sn);
-  } else {
-    for (int idx = lane; idx < k * k; idx += 32) {
-      const int i = idx % k, j = idx / k;
-      Rw[i + j * MMAX] = p.st->R[i + j * MMAX];
-    }
-    __syncwarp();
+  const Factors& F = p.st->f[p.ver];
+  // R' = QRDelete(R) precomputed with this version (recycle), else R itself
+  const double* Rsrc = p.recycle ? F.Rdel : F.R;
+  for (int idx = lane; idx < k * k; idx += 32) {
+    const int i = idx % k, j = idx / k;
+    Rw[i + j * MMAX] = Rsrc[i + j * MMAX];
   }
+  __syncwarp();
   if (p.flags & F_DELETE_ONLY) {
     if (p.variant == V_ICWY) icwy_assemble_T(p, red0, Tw, k);
     out.K = k;
@@ -170,18 +168,89 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   return out;
 }
 
+// The scalars the last CTA of K4 needs (R_kk and ||Delta f||^2) without the O(m^2) head.
+__device__ K4Head k4_scalars_head(const KParams& p) {
+  K4Head out{};
+  const double* red0 = p.red;
+  const int k = p.k;
+  const double* fin = p.red + p.final_slot * LRED;
+  const double vv = (k == 0) ? red0[1] : fin[0];
+  out.rkk = sqrt(vv);
+  out.df2 = red0[1];
+  out.K = k + 1;
+  return out;
+}
+
+// CTA 0 of K4 (warp 0): write factor version ver^1 from the head's results in shared
+// memory (Rw, Tw in scratch; gamma in H.coef).
+__device__ void k4_write_next(const KParams& p, HeadArea& H, const double* scratch, const K4Head& hd) {
+  const int lane = threadIdx.x & 31;
+  const double* Rw = scratch;
+  const double* Tw = scratch + MMAX * MMAX;
+  const Factors& Fi = p.st->f[p.ver];
+  Factors& Fo = p.st->f[p.ver ^ 1];
+  const int K = hd.K;
+  const bool del_only = p.flags & F_DELETE_ONLY;
+  const int mm = p.m;
+  for (int idx = lane; idx < mm * mm; idx += 32) {
+    const int i = idx % mm, j = idx / mm;
+    Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * MMAX] : 0.0;
+    if (p.variant == V_ICWY) {
+      double v = 0.0;
+      if (i == j) v = (i < K) ? 1.0 : 0.0;
+      else if (j < i && i < p.k) v = Tw[i + j * MMAX];
+      Fo.T[i + j * MMAX] = v;
+    }
+  }
+  for (int j = lane; j < p.m; j += 32) {
+    double s = Fi.scale[j];
+    if (p.recycle && j < p.k) s = 1.0;
+    if (!del_only) {
+      if (j == p.k) s = 1.0 / hd.rkk;
+      if (p.variant == V_DCGS2 && p.reortho && j == p.k - 1) s = 1.0;
+    }
+    if (j >= K) s = 1.0;
+    Fo.scale[j] = s;
+    Fo.gamma[j] = del_only ? 0.0 : ((j < K) ? H.coef[j] : 0.0);
+  }
+  if (lane == 0) {
+    Fo.K = K;
+    Fo.has_del = 0;
+  }
+  __syncwarp();
+}
+
+// CTA 0 of K4 (warp 0), after its tiles: QRDelete of the new R, stored
+// with the version so the next recycle step's heads only load it.
+__device__ void k4_precompute_delete(const KParams& p, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  Factors& Fo = p.st->f[p.ver ^ 1];
+  __threadfence_block();
+  const int K = Fo.K;
+  if (K >= 1) {
+    k3_givens_delete(Fo.R, K, scratch, Fo.cs, Fo.sn);
+    const int mm = p.m;
+    for (int idx = lane; idx < mm * mm; idx += 32) {
+      const int i = idx % mm, j = idx / mm;
+      Fo.Rdel[i + j * MMAX] = (i < K - 1 && j < K - 1) ? scratch[i + j * MMAX] : 0.0;
+    }
+  }
+  if (lane == 0) Fo.has_del = 1;
+  __syncwarp();
+}
+
 template <int OP>
 __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
   const int lane = threadIdx.x & 31;
   const double* red0 = p.red;
   const int k = p.k;
   if constexpr (OP == OP_K1) {
-    if (p.recycle) k3_givens_delete(p.st->R, p.c_in, scratch, H.cs, H.sn);
-    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->scale[j];
+    const Factors& F = p.st->f[p.ver];
+    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = F.scale[j];
     __syncwarp();
-    if (p.recycle)
+    if (p.recycle)   // Givens coefficients of QRDelete(R), precomputed by the previous K4
       for (int j = lane; j < p.c_in - 1; j += 32) {
-        const double c = H.cs[j], s = H.sn[j], scn = H.sc[j + 1];
+        const double c = F.cs[j], s = F.sn[j], scn = H.sc[j + 1];
         H.rot[2 * j] = make_double2(c, s * scn);
         H.rot[2 * j + 1] = make_double2(-s, c * scn);
       }
@@ -244,7 +313,7 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
   } else if constexpr (OP == OP_K4) {
     k4_head(p, H, scratch);
   } else if constexpr (OP == OP_GRAM) {
-    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->scale[j];
+    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = p.st->f[p.ver].scale[j];
   }
   __syncwarp();
 }
@@ -356,7 +425,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   const int k = p.k;
   const int vb = p.vb;
 
-  if (warp == 0) op_head<OP>(p, H, scratch);
+  K4Head hd{};
+  if constexpr (OP == OP_K4) {
+    if (warp == 0) {
+      hd = k4_head(p, H, scratch);
+      if (blockIdx.x == 0) k4_write_next(p, H, scratch, hd);
+    }
+  } else {
+    if (warp == 0) op_head<OP>(p, H, scratch);
+  }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], NWARP);
     fence_mbar_init();
@@ -678,6 +755,14 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   }
 
+  if constexpr (OP == OP_K4) {
+    // CTA 0: precompute QRDelete(R_new) for the next step (Givens + re-triangularised R)
+    if (blockIdx.x == 0) {
+      __syncthreads();
+      if (warp == 0) k4_precompute_delete(p, scratch);
+    }
+  }
+
   // ------------------------------------------------------------ cross-CTA reduction
   __threadfence();
   __syncthreads();
@@ -696,52 +781,18 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   }
   __syncthreads();
   if constexpr (OP == OP_K4) {
-    // commit the replicated small factors (only this CTA writes them; every other CTA
-    // has finished reading them)
-    if (warp == 0) {
-      double* Rw = scratch;
-      double* Tw = scratch + MMAX * MMAX;
-      const K4Head hd = k4_head(p, H, scratch);
-      const int K = hd.K;
+    // run-time scalars (the factors were written by CTA 0 from its head)
+    if (tid == 0 && !(p.flags & F_DELETE_ONLY)) {
       SmallState* st = p.st;
-      for (int idx = lane; idx < MMAX * MMAX; idx += 32) {
-        const int i = idx % MMAX, j = idx / MMAX;
-        if (i < p.m && j < p.m) st->R[idx] = (i < K && j < K) ? Rw[i + j * MMAX] : 0.0;
-      }
-      if (p.variant == V_ICWY) {
-        for (int idx = lane; idx < MMAX * MMAX; idx += 32) {
-          const int i = idx % MMAX, j = idx / MMAX;
-          if (i < p.m && j < p.m) {
-            double v = 0.0;
-            if (i == j) v = (i < K) ? 1.0 : 0.0;
-            else if (j < i && i < p.k) v = Tw[i + j * MMAX];
-            st->T[idx] = v;
-          }
-        }
-      }
-      for (int j = lane; j < p.m; j += 32) {
-        double s = st->scale[j];
-        if (p.recycle && j < p.k) s = 1.0;
-        if (!(p.flags & F_DELETE_ONLY)) {
-          if (j == p.k) s = 1.0 / hd.rkk;
-          if (p.variant == V_DCGS2 && p.reortho && j == p.k - 1) s = 1.0;
-        }
-        if (j >= K) s = 1.0;
-        st->scale[j] = s;
-      }
-      if (!(p.flags & F_DELETE_ONLY)) {
-        for (int j = lane; j < MMAX; j += 32) st->gamma[j] = (j < K) ? H.coef[j] : 0.0;
-        if (lane == 0) {
-          st->last_rkk = hd.rkk;
-          const double dfn = sqrt(hd.df2);
-          const double ratio = dfn > 0.0 ? hd.rkk / dfn : 0.0;
-          if (ratio < st->rratio_min) st->rratio_min = ratio;
-          if (!(hd.rkk > p.eps_a * dfn)) st->breakdown = 1;   // reading A12
-          if (!(p.flags & F_EXT_DF)) {
-            st->f2 = p.red[0];
-            st->dx2_local = outv[0];
-          }
-        }
+      hd = k4_scalars_head(p);
+      st->last_rkk = hd.rkk;
+      const double dfn = sqrt(hd.df2);
+      const double ratio = dfn > 0.0 ? hd.rkk / dfn : 0.0;
+      if (ratio < st->rratio_min) st->rratio_min = ratio;
+      if (!(hd.rkk > p.eps_a * dfn)) st->breakdown = 1;   // reading A12
+      if (!(p.flags & F_EXT_DF)) {
+        st->f2 = p.red[0];
+        st->dx2_local = outv[0];
       }
     }
   }
@@ -780,12 +831,12 @@ __global__ void aa_init_kernel(const double* __restrict__ x0, const double* gx0,
 }
 
 // normalised copy of the active Q columns (aa_get_q)
-__global__ void aa_copy_q_kernel(const double* Q, long long ld, const SmallState* st, int mi,
+__global__ void aa_copy_q_kernel(const double* Q, long long ld, const SmallState* st, int ver, int mi,
                                  double* out, long long n) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n * mi;
        idx += (long long)gridDim.x * blockDim.x) {
     const long long j = idx / n, i = idx % n;
-    out[idx] = Q[j * ld + i] * st->scale[j];
+    out[idx] = Q[j * ld + i] * st->f[ver].scale[j];
   }
 }
 

@@ -77,6 +77,7 @@ struct aa_ctx {
   // window bookkeeping (host; depends only on i, m_i)
   int64_t iter = 0;
   int mi = 0, dg_head = 0;
+  int ver = 0;  // factor version read by the next step (K4 writes ver ^ 1)
   bool inited = false;
   int failed = AA_OK;
   // options
@@ -344,6 +345,7 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   for (int i = 0; i < in.nvec; ++i) p.vec[i] = in.vec[i];
   const size_t smem = 0;
   p.st = c->st;
+  p.ver = c->ver;
   p.red = c->red;
   p.part = c->part;
   p.Q = c->Q;
@@ -575,6 +577,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     }
     RET_IF(launch_op<OP_K4>(c, q, in, 2));
   }
+  c->ver ^= 1;
   c->mi = k + 1;
   // ---------------- ledger (paper's logical counts)
   int add;
@@ -737,15 +740,25 @@ int aa_set_option(aa_handle_t h, int opt, double val) {
   }
 }
 
+static void init_small(SmallState* hs, bool keep_scalars, const SmallState* old) {
+  memset(hs, 0, sizeof(SmallState));
+  for (int v = 0; v < 2; ++v)
+    for (int j = 0; j < MMAX; ++j) hs->f[v].scale[j] = 1.0;
+  hs->rratio_min = DBL_MAX;
+  if (keep_scalars && old) {
+    hs->dx2_local = old->dx2_local;
+    hs->f2 = old->f2;
+  }
+}
+
 static int reset_small(aa_ctx* c) {
   SmallState* hs = new SmallState();
-  memset(hs, 0, sizeof(SmallState));
-  for (int j = 0; j < MMAX; ++j) hs->scale[j] = 1.0;
-  hs->rratio_min = DBL_MAX;
+  init_small(hs, false, nullptr);
   cudaError_t e = cudaMemcpyAsync(c->st, hs, sizeof(SmallState), cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   delete hs;
   if (e != cudaSuccess) return fail(c, AA_ERR_CUDA);
+  c->ver = 0;
   return AA_OK;
 }
 
@@ -836,6 +849,7 @@ int aa_delete_oldest(aa_handle_t h) {
     q.flags |= F_COMMIT_ONLY;
     RET_IF(launch_op<OP_K4>(h, q, Inputs(), 2));
   }
+  h->ver ^= 1;
   h->mi = k;
   h->dg_head = (h->dg_head + 1) % h->m;
   h->logical_last[AA_PH_QRDELETE] = (V == V_ICWY) ? 1 : 0;
@@ -933,18 +947,17 @@ int aa_reset(aa_handle_t h) {
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->mi = 0;
   h->dg_head = 0;
+  SmallState* old = new SmallState();
   SmallState* hs = new SmallState();
-  memset(hs, 0, sizeof(SmallState));
-  for (int j = 0; j < MMAX; ++j) hs->scale[j] = 1.0;
-  hs->rratio_min = DBL_MAX;
-  // keep dx2_local / f2
-  cudaError_t e = cudaMemcpy(h->st, hs, offsetof(SmallState, dx2_local), cudaMemcpyHostToDevice);
-  int bd = 0;
-  if (e == cudaSuccess)
-    e = cudaMemcpy(reinterpret_cast<char*>(h->st) + offsetof(SmallState, breakdown), &bd, sizeof(int),
-                   cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMemcpy(old, h->st, sizeof(SmallState), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) {
+    init_small(hs, true, old);   // keep ||dx||^2 / ||f||^2 of the last step
+    e = cudaMemcpy(h->st, hs, sizeof(SmallState), cudaMemcpyHostToDevice);
+  }
+  delete old;
   delete hs;
   if (e != cudaSuccess) return fail(h, AA_ERR_CUDA);
+  h->ver = 0;
   return AA_OK;
 }
 
@@ -982,15 +995,16 @@ int aa_get_small(aa_handle_t h, double* R, double* T, double* gamma, double* sca
     return fail(h, AA_ERR_CUDA);
   }
   const int m = h->m;
+  const Factors& F = hs->f[h->ver];
   for (int j = 0; j < m; ++j)
     for (int i = 0; i < m; ++i) {
-      if (R) R[i + j * m] = hs->R[i + j * MMAX];
-      if (T) T[i + j * m] = hs->T[i + j * MMAX];
+      if (R) R[i + j * m] = F.R[i + j * MMAX];
+      if (T) T[i + j * m] = F.T[i + j * MMAX];
     }
   if (gamma)
-    for (int j = 0; j < h->mi; ++j) gamma[j] = hs->gamma[j];
+    for (int j = 0; j < h->mi; ++j) gamma[j] = F.gamma[j];
   if (scale)
-    for (int j = 0; j < m; ++j) scale[j] = hs->scale[j];
+    for (int j = 0; j < m; ++j) scale[j] = F.scale[j];
   delete hs;
   return AA_OK;
 }
@@ -999,7 +1013,7 @@ int aa_get_q(aa_handle_t h, double* q_out) {
   RET_IF(check_handle(h));
   if (!q_out) return AA_ERR_ARG;
   if (h->mi == 0) return AA_OK;
-  aa_copy_q_kernel<<<h->sms * 4, 256, 0, h->stream>>>(h->Q, h->ld, h->st, h->mi, q_out, h->n);
+  aa_copy_q_kernel<<<h->sms * 4, 256, 0, h->stream>>>(h->Q, h->ld, h->st, h->ver, h->mi, q_out, h->n);
   h->launches++;
   CUDA_TRY(h, cudaGetLastError());
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
