@@ -244,24 +244,19 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const bool skew = (G > 0);
   const bool vec_only = (p.nblk == 0 && p.nin > 0);
   const int nin = std::max(p.nin, 1);
+  // Tile policy (tools/tune_tiles.sh sweeps, config 2, m in {5,10,20,50}):
+  // the largest tile (256 rows; 252 with a Gram; 1024 for vector-only kernels) with a
+  // 2-stage ring; kernels other than K1 whose tile is small (few columns) take more
+  // stages (~96 KB per CTA) while two CTAs still fit on an SM.
   int tr = 0, stages = 0;
-  bool ok = false;
-  if (regs <= 128) {
-    if (OP == OP_K1 && !skew)  // K1 without a Gram: largest tile that still gets 4 stages
-      ok = choose_tile(nin, skew, vec_only, 104 * 1024, 4, 4, 256, &tr, &stages);
-    if (!ok) {
-      // 2 stages of the largest tile; more stages only when the tile is small (few columns)
-      ok = choose_tile(nin, skew, vec_only, 104 * 1024, 2, MAXSTAGES, vec_only ? 1024 : 256, &tr, &stages);
-      if (ok && !vec_only) {
-        const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
-        stages = (int)std::max<size_t>(2, std::min<size_t>(MAXSTAGES, (96 * 1024 + sb - 1) / sb));
-        if ((size_t)stages * sb > 104 * 1024) stages = (int)((104 * 1024) / sb);
-      } else if (ok) {
-        stages = 2;
-      }
+  choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, vec_only ? 1024 : 256, &tr, &stages);
+  if (OP != OP_K1 && regs <= 128) {
+    const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
+    if (2 * sb <= 104 * 1024) {
+      stages = (int)std::max<size_t>(2, std::min<size_t>(MAXSTAGES, (96 * 1024 + sb - 1) / sb));
+      while (stages > 2 && (size_t)stages * sb > 104 * 1024) --stages;
     }
   }
-  if (!ok) choose_tile(nin, skew, vec_only, 200 * 1024, 2, 3, 1024, &tr, &stages);
   // tuning override (tools only): AA_TILE="<op>:<tr>:<stages>[,<op>:<tr>:<stages>...]"
   if (const char* ov = getenv("AA_TILE")) {
     const char* q = ov;
