@@ -109,6 +109,7 @@ struct alignas(64) KParams {
   int words;        // words this kernel reduces
   int nin, tr, stages;
   int vb;           // first vector column (= sum of block columns)
+  int tm3d;         // column blocks use 3-D maps (TR a multiple of 256)
   int beta_on;
   long long n;      // local rows
   double beta, eps_a;
@@ -169,6 +170,15 @@ __device__ __forceinline__ void tma_2d_g2s(void* dst, const CUtensorMap* map, in
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA 3-D tensor copy: Q viewed as {256 rows, row block, column}; one box brings TR =
+// 256*k rows x ncols columns into the [column][TR] stage layout.
+__device__ __forceinline__ void tma_3d_g2s(void* dst, const CUtensorMap* map, int rblk, int col, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(rblk), "r"(col), "r"(smem_u32(bar))
       : "memory");
 }
 // fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col)

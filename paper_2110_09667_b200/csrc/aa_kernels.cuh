@@ -337,7 +337,10 @@ __device__ void issue_tile_part(const KParams& p, double* stage, uint64_t* bar, 
     if (c < p.nblk) {
       int col0 = 0;
       for (int b = 0; b < c; ++b) col0 += p.blk_ncols[b];
-      tma_2d_g2s(stage + (size_t)col0 * TR, &p.tm[c], (int)row0, p.blk_gcol[c], bar);
+      if (p.tm3d)
+        tma_3d_g2s(stage + (size_t)col0 * TR, &p.tm[c], (int)(row0 >> 8), p.blk_gcol[c], bar);
+      else
+        tma_2d_g2s(stage + (size_t)col0 * TR, &p.tm[c], (int)row0, p.blk_gcol[c], bar);
     } else {
       const int i = c - p.nblk;
       const uint32_t b = vec_bytes(p, i, rows);

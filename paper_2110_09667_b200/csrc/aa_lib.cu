@@ -78,6 +78,7 @@ struct aa_ctx {
   int64_t iter = 0;
   int mi = 0, dg_head = 0;
   int ver = 0;  // factor version read by the next step (K4 writes ver ^ 1)
+  int max_tr_blocks = 512;  // tallest tile for kernels with column blocks
   bool inited = false;
   int failed = AA_OK;
   // options
@@ -129,10 +130,10 @@ double* dgcol(aa_ctx* c, int slot) { return c->DG + (size_t)slot * c->ld; }
 bool choose_tile(int nin, bool skew, bool vec_only, size_t budget, int min_stages, int max_stages, int max_tr,
                  int* tr, int* stages) {
   static const int trs_s[] = {252, 124, 60, 28};
-  static const int trs_p[] = {256, 128, 64, 32};
+  static const int trs_p[] = {1024, 512, 256, 128, 64, 32};
   static const int trs_v[] = {1024, 512, 256, 128, 64, 32};
   const int* trs = skew ? trs_s : (vec_only ? trs_v : trs_p);
-  const int nt = vec_only ? 6 : 4;
+  const int nt = skew ? 4 : 6;
   for (int t = 0; t < nt; ++t) {
     if (trs[t] > max_tr) continue;
     const size_t sb = align_up((size_t)nin * trs[t], 16) * sizeof(double);
@@ -170,13 +171,25 @@ const CUtensorMap* get_map(aa_ctx* c, int which, int ncols, int tr) {
   auto fn = encode_fn();
   if (!fn) return nullptr;
   CUtensorMap m;
-  cuuint64_t gdim[2] = {(cuuint64_t)c->n, (cuuint64_t)c->m};
-  cuuint64_t gstr[1] = {(cuuint64_t)(c->ld * sizeof(double))};
-  cuuint32_t box[2] = {(cuuint32_t)tr, (cuuint32_t)ncols};
-  cuuint32_t es[2] = {1, 1};
   void* base = which == 0 ? (void*)c->Q : (void*)c->DG;
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (tr % 256 == 0) {
+    // 3-D view {256 rows, ld/256 row blocks, m columns}: a box of tr/256 row blocks; the
+    // padding rows [n, ld) are zero (never written), row blocks past ld are zero-filled
+    cuuint64_t gdim[3] = {256, (cuuint64_t)(c->ld / 256), (cuuint64_t)c->m};
+    cuuint64_t gstr[2] = {256 * sizeof(double), (cuuint64_t)(c->ld * sizeof(double))};
+    cuuint32_t box[3] = {256, (cuuint32_t)(tr / 256), (cuuint32_t)ncols};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t gdim[2] = {(cuuint64_t)c->n, (cuuint64_t)c->m};
+    cuuint64_t gstr[1] = {(cuuint64_t)(c->ld * sizeof(double))};
+    cuuint32_t box[2] = {(cuuint32_t)tr, (cuuint32_t)ncols};
+    cuuint32_t es[2] = {1, 1};
+    r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) {
     fprintf(stderr, "libaa: cuTensorMapEncodeTiled failed (%d) for %d cols x %d rows\n", (int)r, ncols, tr);
     return nullptr;
@@ -245,17 +258,21 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const bool vec_only = (p.nblk == 0 && p.nin > 0);
   const int nin = std::max(p.nin, 1);
   // Tile policy (tools/tune_tiles.sh sweeps, config 2, m in {5,10,20,50}):
-  // the largest tile (256 rows; 252 with a Gram; 1024 for vector-only kernels) with a
-  // 2-stage ring; kernels other than K1 whose tile is small (few columns) take more
-  // stages (~96 KB per CTA) while two CTAs still fit on an SM.
+  // the tallest tile (<= 512 rows for column-block kernels via 3-D tensor maps; 252 with a
+  // DMMA Gram; 1024 for vector-only kernels) whose 2-stage ring fits one CTA's shared
+  // memory; then as many extra stages (<= 4) as fit while two CTAs share an SM (when the
+  // registers allow) -- small tiles (few columns) need them to keep bytes in flight.
   int tr = 0, stages = 0;
-  choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, vec_only ? 1024 : 256, &tr, &stages);
-  if (OP != OP_K1 && regs <= 128) {
+  bool k1_two = false;
+  if (OP == OP_K1 && !skew && nin < 20 && regs <= 128)
+    // K1 with few columns: keep two CTAs per SM (16 warps hide the rotation chain)
+    k1_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, c->max_tr_blocks, &tr, &stages) && tr >= 256;
+  if (!k1_two)
+    choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, vec_only ? 1024 : c->max_tr_blocks, &tr, &stages);
+  if (OP != OP_K1) {
     const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
-    if (2 * sb <= 104 * 1024) {
-      stages = (int)std::max<size_t>(2, std::min<size_t>(MAXSTAGES, (96 * 1024 + sb - 1) / sb));
-      while (stages > 2 && (size_t)stages * sb > 104 * 1024) --stages;
-    }
+    const size_t budget = (regs <= 128 && 2 * sb <= 104 * 1024) ? 104 * 1024 : 0;
+    if (budget) stages = (int)std::max<size_t>(2, std::min<size_t>(4, budget / sb));
   }
   // tuning override (tools only): AA_TILE="<op>:<tr>:<stages>[,<op>:<tr>:<stages>...]"
   if (const char* ov = getenv("AA_TILE")) {
@@ -276,6 +293,7 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   }
   p.tr = tr;
   p.stages = stages;
+  p.tm3d = (tr % 256 == 0) ? 1 : 0;
   for (int b = 0; b < p.nblk; ++b) {
     const CUtensorMap* m = get_map(c, p.blk_which[b], p.blk_ncols[b], tr);
     if (!m) return fail(c, AA_ERR_CUDA);
