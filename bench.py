@@ -221,6 +221,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    # one JSON line on stdout: keep NCCL's banner (the image sets NCCL_DEBUG=VERSION) off it
+    os.environ["NCCL_DEBUG"] = os.environ.get("AA_NCCL_DEBUG", "WARN")
     import torch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
