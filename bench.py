@@ -193,7 +193,7 @@ def _config(args):
                          f"{args.variant.upper()} RECYCLE aa_step (QRDelete+QRAdd+LSP+update), "
                          "G(x)=d*x+b, d~U[-0.9,0.9), b~U[-1,1) (SplitMix64 seed 9667), x0=0"),
             "n_local": int(args.n_local), "m": args.m, "variant": args.variant,
-            "parallelism": f"rows{args.gpus}", "l2": "inputs larger than L2 (0.8 GB per vector)",
+            "parallelism": f"rows{args.gpus}", "allreduce": "fused NVLink one-shot" if args.fused_ar else "ncclAllReduce", "l2": "inputs larger than L2 (0.8 GB per vector)",
             "timed": "aa_step only (CUDA events on the handle's stream); G excluded"}
 
 
@@ -215,6 +215,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--only-headline", action="store_true")
     ap.add_argument("--icwy-merged", type=int, default=0)
+    ap.add_argument("--fused-ar", type=int, default=0,
+                    help="1: one-shot NVLink exchange in the kernel's last CTA instead of ncclAllReduce")
     args = ap.parse_args()
     args.steps = max(1, args.steps)
     args.warmup = max(3, args.warmup)
@@ -265,7 +267,8 @@ def main():
     def measure(variant, m, steps, warmup, with_clocks=False, e2e=False):
         s = aa.AndersonSolver(n_local, m, variant, rank=rank, nranks=world, unique_id=uid,
                               nccl_comm=comm, stream=stream, profile=1, n_global=n_local * world,
-                              icwy_merged=args.icwy_merged)
+                              icwy_merged=args.icwy_merged,
+                              fused_allreduce=1 if (args.fused_ar and world > 1) else None)
         x = torch.zeros(n_local, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)
         s.init(x, G(x), xn)
@@ -340,7 +343,7 @@ def main():
         aa.aa_fill_uniform(bn, nl, -1.0, 1.0, stream_id=2, offset=rank * nl, stream=stream)
         Gn = lambda x: torch.addcmul(bn, dn, x)
         s = aa.AndersonSolver(nl, m, variant, rank=rank, nranks=world, nccl_comm=comm, stream=stream,
-                              n_global=nl * world)
+                              n_global=nl * world, fused_allreduce=1 if (args.fused_ar and world > 1) else None)
         x = torch.zeros(nl, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)
         s.init(x, Gn(x), xn)

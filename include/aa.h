@@ -81,7 +81,11 @@ enum aa_option {
     AA_OPT_DCGS2_RSCALE = 3,   /* 0 = R += s verbatim (Alg. 6 l.5); 1 = R += R_kk s (A3)  */
     AA_OPT_BREAKDOWN_EPS = 4,  /* eps_a; default 10 * DBL_EPSILON * sqrt(n_global)        */
     AA_OPT_PROFILE = 5,        /* 1 = record per-kernel CUDA events (aa_timings)           */
-    AA_OPT_N_GLOBAL = 6        /* global vector length (for the default eps_a)             */
+    AA_OPT_N_GLOBAL = 6,       /* global vector length (for the default eps_a)             */
+    AA_OPT_FUSED_ALLREDUCE = 7 /* 1 = every global reduction is a one-shot exchange done by
+                                  the producing kernel's last CTA over NVLink peer memory
+                                  (CUDA IPC, same node) instead of ncclAllReduce; collective
+                                  (all ranks set it); 0 = ncclAllReduce (default)          */
 };
 
 /* aa_stats flags */

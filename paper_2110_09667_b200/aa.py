@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libaa.so")
 MGS, ICWY, CGS2, DCGS2 = 0, 1, 2, 3
 VARIANT_IDS = {"mgs": MGS, "icwy": ICWY, "cgs2": CGS2, "dcgs2": DCGS2}
 OPT_DAMPING_BETA, OPT_ICWY_DELETE, OPT_DCGS2_COND, OPT_DCGS2_RSCALE = 0, 1, 2, 3
-OPT_BREAKDOWN_EPS, OPT_PROFILE, OPT_N_GLOBAL = 4, 5, 6
+OPT_BREAKDOWN_EPS, OPT_PROFILE, OPT_N_GLOBAL, OPT_FUSED_ALLREDUCE = 4, 5, 6, 7
 STATS_LOO, STATS_RESET = 1, 2
 AA_OK, AA_ERR_BREAKDOWN = 0, 6
 PHASES = ("qradd", "qrdelete", "lsp_rhs", "norm_check", "other")
@@ -255,7 +255,7 @@ class AndersonSolver:
             self.h = aa_create(n_local, m, variant, rank, nranks, unique_id, stream)
         names = {"beta": OPT_DAMPING_BETA, "icwy_merged": OPT_ICWY_DELETE, "dcgs2_cond": OPT_DCGS2_COND,
                  "dcgs2_rscale": OPT_DCGS2_RSCALE, "breakdown_eps": OPT_BREAKDOWN_EPS,
-                 "profile": OPT_PROFILE, "n_global": OPT_N_GLOBAL}
+                 "profile": OPT_PROFILE, "n_global": OPT_N_GLOBAL, "fused_allreduce": OPT_FUSED_ALLREDUCE}
         for k, v in options.items():
             if v is not None:
                 aa_set_option(self.h, names[k], float(v))

@@ -60,6 +60,7 @@ struct SmallState {
   double last_rkk;
   int breakdown;             // sticky
   unsigned int counter;      // cross-CTA arrival ticket
+  int xchg_timeout;          // sticky: a fused peer exchange timed out
 };
 
 // K1 reduction-slot layout (words), identical on host and device.
@@ -79,6 +80,7 @@ struct K1Layout {
 };
 
 constexpr int NVEC_MAX = 8;   // 1-D vector streams per kernel
+constexpr int MAX_RANKS = 8;  // fused NVLink exchange: ranks of one node
 constexpr int NBLK_MAX = 3;   // 2-D column blocks (tensor maps) per kernel
 
 // Kernel parameters.  Inputs of one tile are staged in shared memory as columns:
@@ -121,6 +123,16 @@ struct alignas(64) KParams {
   double* x_out;    // K4 output
   SmallState* st;
   int ver;          // factor version read by this step (written: ver ^ 1, by K4)
+  // fused one-shot allreduce over NVLink peer memory (AA_OPT_FUSED_ALLREDUCE): the last
+  // CTA exchanges words [xoff[e], xoff[e]+xcnt[e]) of its reduction slot, e < nxchg,
+  // with sequence numbers seq0 + e
+  int nxchg, nranks, rank;
+  int xoff[2], xcnt[2];
+  unsigned long long seq0;
+  double* pmbox[MAX_RANKS];               // peer q's mailbox (q == rank: local)
+  unsigned long long* pflags[MAX_RANKS];  // peer q's flag array
+  double* lmbox;
+  unsigned long long* lflags;
   double* red;      // reduction slots (slot s at red + s*LRED)
   double* part;     // per-CTA partials (CTA b at part + b*LRED)
 };

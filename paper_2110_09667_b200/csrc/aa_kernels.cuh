@@ -408,6 +408,60 @@ __device__ void gram_epilogue(const KParams& p, const double* gc0, const double*
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------- fused allreduce
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One-shot allreduce of v[0..cnt) among the node's ranks, run by the LAST CTA of a kernel
+// on every rank ("fused local + global reduction"):
+// push v into slot [seq&1][rank] of every peer's mailbox through NVLink, publish seq in
+// the peer's flag[rank] (release, system scope), wait until every flag[q] >= seq
+// (acquire), then sum the p vectors in rank order -- the same order on every rank, so all
+// ranks obtain bitwise identical sums.  Double-buffered by seq parity: a peer reaches
+// seq+2 only after this rank has published seq+1, i.e. after it finished reading seq.
+// The wait is time-bounded (10 s): on timeout a sticky flag is set instead of hanging.
+__device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned long long seq) {
+  const int tid = threadIdx.x;
+  const int par = (int)(seq & 1ull);
+  const size_t slot = (size_t)(par * p.nranks + p.rank) * LRED;
+  for (int q = 0; q < p.nranks; ++q) {
+    double* dst = p.pmbox[q] + slot;
+    for (int w = tid; w < cnt; w += NT) dst[w] = v[w];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (int q = 0; q < p.nranks; ++q) st_release_sys(p.pflags[q] + p.rank, seq);
+  }
+  if (tid < p.nranks) {
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(p.lflags + tid) < seq) {
+      if (global_ns() - t0 > 10000000000ull) {
+        p.st->xchg_timeout = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  for (int w = tid; w < cnt; w += NT) {
+    double s = 0.0;
+    for (int q = 0; q < p.nranks; ++q) s += __ldcg(p.lmbox + (size_t)(par * p.nranks + q) * LRED + w);
+    v[w] = s;
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------- kernel
 // OP: the op; NCW: phase-B columns per warp (0 = no block multi-dot); NB8: 8-column
 // groups of the DMMA Gram (0 = no Gram).
@@ -783,6 +837,9 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     outv[w] = s;
   }
   __syncthreads();
+  if constexpr (OP != OP_K4) {
+    for (int e = 0; e < p.nxchg; ++e) fused_exchange(p, outv + p.xoff[e], p.xcnt[e], p.seq0 + e);
+  }
   if constexpr (OP == OP_K4) {
     // run-time scalars (the factors were written by CTA 0 from its head)
     if (tid == 0 && !(p.flags & F_DELETE_ONLY)) {

@@ -33,6 +33,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -49,6 +50,7 @@ NcclApi& nccl() {
   api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
   api.AllReduce = (decltype(api.AllReduce))dlsym(lib, "ncclAllReduce");
+  api.AllGather = (decltype(api.AllGather))dlsym(lib, "ncclAllGather");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(lib, "ncclGetErrorString");
   api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
@@ -79,6 +81,11 @@ struct aa_ctx {
   int mi = 0, dg_head = 0;
   int ver = 0;  // factor version read by the next step (K4 writes ver ^ 1)
   int max_tr_blocks = 512;  // tallest tile for kernels with column blocks
+  // fused one-shot NVLink allreduce (AA_OPT_FUSED_ALLREDUCE)
+  int fused = 0;
+  void* xbuf = nullptr;                 // local [flags 4 KB][mailbox 2 x nranks x LRED]
+  void* peer_base[MAX_RANKS] = {};
+  unsigned long long seq = 0;
   bool inited = false;
   int failed = AA_OK;
   // options
@@ -416,6 +423,12 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   }
 }
 
+#define RET_IF_(x)              \
+  do {                          \
+    int _s = (x);               \
+    if (_s != AA_OK) return _s; \
+  } while (0)
+
 int allreduce(aa_ctx* c, double* buf, size_t count) {
   if (c->nranks == 1 || count == 0) return AA_OK;
   EvScope ev(c, 3);
@@ -427,6 +440,43 @@ int allreduce(aa_ctx* c, double* buf, size_t count) {
   }
   c->ar_last++;
   c->ar_total++;
+  return AA_OK;
+}
+
+constexpr size_t kFlagBytes = 4096;
+
+// Plan the reduction(s) at the end of the kernel q: ranges [o0, o0+n0) and [o1, o1+n1) of
+// its reduction slot, each ONE global reduction (n = 0: none).  Fused mode: the kernel's
+// last CTA exchanges them over NVLink; otherwise post_ar() issues ncclAllReduce after it.
+void plan_ar(aa_ctx* c, KParams& q, int o0, int n0, int o1, int n1) {
+  q.nxchg = 0;
+  if (!(c->fused && c->nranks > 1)) return;
+  const int offs[2] = {o0, o1}, cnts[2] = {n0, n1};
+  q.nranks = c->nranks;
+  q.rank = c->rank;
+  q.seq0 = c->seq + 1;
+  for (int e = 0; e < 2; ++e)
+    if (cnts[e] > 0) {
+      q.xoff[q.nxchg] = offs[e];
+      q.xcnt[q.nxchg] = cnts[e];
+      ++q.nxchg;
+    }
+  c->seq += q.nxchg;
+  for (int r = 0; r < c->nranks; ++r) {
+    q.pflags[r] = (unsigned long long*)c->peer_base[r];
+    q.pmbox[r] = (double*)((char*)c->peer_base[r] + kFlagBytes);
+  }
+  q.lflags = (unsigned long long*)c->xbuf;
+  q.lmbox = (double*)((char*)c->xbuf + kFlagBytes);
+  c->ar_last += q.nxchg;
+  c->ar_total += q.nxchg;
+}
+
+int post_ar(aa_ctx* c, double* slot, int o0, int n0, int o1, int n1) {
+  c->sp_last += (n0 > 0) + (n1 > 0);
+  if (c->fused || c->nranks == 1) return AA_OK;
+  if (n0 > 0) RET_IF_(allreduce(c, slot + o0, (size_t)n0));
+  if (n1 > 0) RET_IF_(allreduce(c, slot + o1, (size_t)n1));
   return AA_OK;
 }
 
@@ -483,6 +533,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   p.flags = ext ? F_EXT_DF : 0;
 
   // ---------------- K1: prologue + QRDelete rotation + pass-1 multi-dot
+  int k1_ar[4];
   {
     KParams q = p;
     q.op = OP_K1;
@@ -500,18 +551,16 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     q.dg_out = dgcol(c, dg_slot);
     q.words = L.words;
     q.red_slot = 0;
+    // the ICWY correction-matrix update after QRDelete is its own reduction
+    if (gram && L.n_gram > 0 && !c->icwy_merged) {
+      k1_ar[0] = L.off_gram; k1_ar[1] = L.n_gram; k1_ar[2] = 0; k1_ar[3] = L.off_gram;
+    } else {
+      k1_ar[0] = 0; k1_ar[1] = L.words; k1_ar[2] = 0; k1_ar[3] = 0;
+    }
+    plan_ar(c, q, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]);
     RET_IF(launch_op<OP_K1>(c, q, in, 0));
   }
-  if (gram && L.n_gram > 0 && !c->icwy_merged) {
-    // the ICWY correction-matrix update after QRDelete: its own reduction
-    RET_IF(allreduce(c, c->red + L.off_gram, (size_t)L.n_gram));
-    c->sp_last++;
-    RET_IF(allreduce(c, c->red, (size_t)L.off_gram));
-    c->sp_last++;
-  } else {
-    RET_IF(allreduce(c, c->red, (size_t)L.words));
-    c->sp_last++;
-  }
+  RET_IF(post_ar(c, c->red, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]));
   // ---------------- K2: the rest of QRAdd
   int final_slot = 0;
   if (k >= 1) {
@@ -523,10 +572,10 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
       in.vector(c->fp, false);            // f_i
       q.words = 2;
       q.red_slot = 1;
+      plan_ar(c, q, 0, 2, 0, 0);
       if (V == V_ICWY) RET_IF(launch_op<OP_K2_ICWY>(c, q, in, 1));
       else RET_IF(launch_op<OP_K2_DCGS2>(c, q, in, 1));
-      RET_IF(allreduce(c, c->red + LRED, 2));
-      c->sp_last++;
+      RET_IF(post_ar(c, c->red + LRED, 0, 2, 0, 0));
       final_slot = 1;
     } else if (V == V_CGS2) {
       q.op = OP_K2A_CGS2;
@@ -534,9 +583,9 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
       in.block(0, 0, k + 1);
       q.words = k;
       q.red_slot = 1;
+      plan_ar(c, q, 0, k, 0, 0);
       RET_IF(launch_op<OP_K2A_CGS2>(c, q, in, 1));
-      RET_IF(allreduce(c, c->red + LRED, (size_t)k));
-      c->sp_last++;
+      RET_IF(post_ar(c, c->red + LRED, 0, k, 0, 0));
       KParams q2 = p;
       q2.op = OP_K2B_CGS2;
       Inputs in2;
@@ -544,9 +593,9 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
       in2.vector(c->fp, false);
       q2.words = 2;
       q2.red_slot = 2;
+      plan_ar(c, q2, 0, 2, 0, 0);
       RET_IF(launch_op<OP_K2B_CGS2>(c, q2, in2, 1));
-      RET_IF(allreduce(c, c->red + 2 * LRED, 2));
-      c->sp_last++;
+      RET_IF(post_ar(c, c->red + 2 * LRED, 0, 2, 0, 0));
       final_slot = 2;
     } else {  // MGS: k dependent passes
       for (int j = 1; j <= k; ++j) {
@@ -559,9 +608,9 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
         in.vector((j < k) ? qcol(c, j) : c->fp, false);
         q2.words = (j < k) ? 1 : 2;
         q2.red_slot = j;
+        plan_ar(c, q2, 0, q2.words, 0, 0);
         RET_IF(launch_op<OP_K2_MGS>(c, q2, in, 1));
-        RET_IF(allreduce(c, c->red + (size_t)j * LRED, (size_t)q2.words));
-        c->sp_last++;
+        RET_IF(post_ar(c, c->red + (size_t)j * LRED, 0, q2.words, 0, 0));
       }
       final_slot = k;
     }
@@ -707,6 +756,38 @@ static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant,
   return AA_OK;
 }
 
+// Fused-allreduce setup (collective): one device buffer per rank [flags][mailbox], its
+// CUDA IPC handle all-gathered over the handle's NCCL communicator, peers' buffers
+// opened with cudaIpcOpenMemHandle (NVLink P2P within the node).
+static int fused_setup(aa_ctx* c) {
+  if (c->nranks > MAX_RANKS || !nccl().AllGather) return AA_ERR_ARG;
+  const size_t bytes = kFlagBytes + (size_t)2 * c->nranks * LRED * sizeof(double);
+  CUDA_TRY(c, cudaMalloc(&c->xbuf, bytes));
+  CUDA_TRY(c, cudaMemset(c->xbuf, 0, bytes));
+  cudaIpcMemHandle_t mine;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&mine, c->xbuf));
+  char* dh = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * c->nranks));
+  CUDA_TRY(c, cudaMemcpy(dh + sizeof(mine) * c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  if (nccl().AllGather(dh + sizeof(mine) * c->rank, dh, sizeof(mine), 0 /*ncclInt8*/, c->comm, c->stream) != 0) {
+    cudaFree(dh);
+    return fail(c, AA_ERR_NCCL);
+  }
+  std::vector<cudaIpcMemHandle_t> all(c->nranks);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, cudaMemcpy(all.data(), dh, sizeof(mine) * c->nranks, cudaMemcpyDeviceToHost));
+  cudaFree(dh);
+  for (int r = 0; r < c->nranks; ++r) {
+    if (r == c->rank) {
+      c->peer_base[r] = c->xbuf;
+    } else {
+      CUDA_TRY(c, cudaIpcOpenMemHandle(&c->peer_base[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+    }
+  }
+  c->seq = 0;
+  return AA_OK;
+}
+
 int aa_create(aa_handle_t* out, int64_t n_local, int m, int qr_variant, int rank, int nranks,
               const void* id128, void* cuda_stream) {
   return create_impl(out, n_local, m, qr_variant, rank, nranks, id128, nullptr, cuda_stream);
@@ -747,6 +828,11 @@ int aa_set_option(aa_handle_t h, int opt, double val) {
     case AA_OPT_N_GLOBAL:
       if (!(val >= 1.0)) return AA_ERR_ARG;
       h->n_global = (int64_t)val;
+      return AA_OK;
+    case AA_OPT_FUSED_ALLREDUCE:
+      if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
+      if (val == 1.0 && h->nranks > 1 && !h->xbuf) RET_IF_(fused_setup(h));
+      h->fused = (int)val;
       return AA_OK;
     default:
       return AA_ERR_ARG;
@@ -848,12 +934,10 @@ int aa_delete_oldest(aa_handle_t h) {
     in.block(0, 0, h->mi);
     q.words = words;
     q.red_slot = 0;
+    plan_ar(h, q, 0, V == V_ICWY ? words : 0, 0, 0);
     RET_IF(launch_op<OP_K1>(h, q, in, 0));
   }
-  if (V == V_ICWY) {
-    RET_IF(allreduce(h, h->red, (size_t)words));
-    if (words > 0) h->sp_last++;
-  }
+  if (V == V_ICWY) RET_IF(post_ar(h, h->red, 0, words, 0, 0));
   {
     KParams q = p;
     q.op = OP_K4;
@@ -903,7 +987,12 @@ int aa_stats(aa_handle_t h, struct aa_stats* out, int flags) {
     hs.f2 = full->f2;
     hs.rmin = full->rratio_min;
     hs.bd = full->breakdown;
+    const int xto = full->xchg_timeout;
     delete full;
+    if (xto) {
+      fprintf(stderr, "libaa: fused peer exchange timed out\n");
+      return fail(h, AA_ERR_NCCL);
+    }
     CUDA_TRY(h, e);
   }
   if (h->nranks > 1) {
@@ -981,6 +1070,9 @@ int aa_destroy(aa_handle_t h) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
+  for (int r = 0; r < MAX_RANKS; ++r)
+    if (h->peer_base[r] && h->peer_base[r] != h->xbuf) cudaIpcCloseMemHandle(h->peer_base[r]);
+  cudaFree(h->xbuf);
   if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
   cudaFree(h->Q);
   cudaFree(h->DG);

@@ -16,13 +16,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_multi_gpu_parity_and_allreduce_counts(tmp_path):
+@pytest.mark.parametrize("mode", ["torch_comm", "torch_comm_fused"])
+def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
+    """NCCL allreduce per reduction (torch_comm) or the fused one-shot NVLink exchange in
+    the producing kernel's last CTA (torch_comm_fused)."""
     from aa_inputs import problems
     from oracle import aa_variant
     world = min(torch.cuda.device_count(), 4)
     out = tmp_path / "dist.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
-           f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "_dist_worker.py"), str(out)]
+           f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "_dist_worker.py"), str(out), mode]
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
