@@ -193,7 +193,7 @@ def _config(args):
                          f"{args.variant.upper()} RECYCLE aa_step (QRDelete+QRAdd+LSP+update), "
                          "G(x)=d*x+b, d~U[-0.9,0.9), b~U[-1,1) (SplitMix64 seed 9667), x0=0"),
             "n_local": int(args.n_local), "m": args.m, "variant": args.variant,
-            "parallelism": f"rows{args.gpus}", "allreduce": "fused NVLink one-shot" if args.fused_ar else "ncclAllReduce", "l2": "inputs larger than L2 (0.8 GB per vector)",
+            "parallelism": f"rows{args.gpus}", "l2": "inputs larger than L2 (0.8 GB per vector)",
             "timed": "aa_step only (CUDA events on the handle's stream); G excluded"}
 
 
@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--only-headline", action="store_true")
     ap.add_argument("--icwy-merged", type=int, default=0)
-    ap.add_argument("--fused-ar", type=int, default=0,
+    ap.add_argument("--fused-ar", type=int, default=1,
                     help="1: one-shot NVLink exchange in the kernel's last CTA instead of ncclAllReduce")
     args = ap.parse_args()
     args.steps = max(1, args.steps)
@@ -233,7 +233,18 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # C-level prints during communicator set-up (NCCL's version banner) go to stderr:
+        # stdout carries exactly one JSON line
+        saved_fd = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved_fd, 1)
+            os.close(saved_fd)
     from paper_2110_09667_b200 import aa
 
     uid, comm = None, None
@@ -264,11 +275,21 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    ar_mode = {"mode": "ncclAllReduce" if world > 1 else "none (1 rank)"}
+
+    def make_solver(nl, m, variant, **kw):
+        s = aa.AndersonSolver(nl, m, variant, rank=rank, nranks=world, unique_id=uid, nccl_comm=comm,
+                              stream=stream, n_global=nl * world, **kw)
+        if args.fused_ar and world > 1:
+            try:
+                aa.aa_set_option(s.h, aa.OPT_FUSED_ALLREDUCE, 1)
+                ar_mode["mode"] = "fused one-shot NVLink exchange in the kernel's last CTA"
+            except aa.AAError as e:   # IPC unavailable: NCCL stays in use
+                ar_mode["mode"] = f"ncclAllReduce (fused setup failed: {e})"
+        return s
+
     def measure(variant, m, steps, warmup, with_clocks=False, e2e=False):
-        s = aa.AndersonSolver(n_local, m, variant, rank=rank, nranks=world, unique_id=uid,
-                              nccl_comm=comm, stream=stream, profile=1, n_global=n_local * world,
-                              icwy_merged=args.icwy_merged,
-                              fused_allreduce=1 if (args.fused_ar and world > 1) else None)
+        s = make_solver(n_local, m, variant, profile=1, icwy_merged=args.icwy_merged)
         x = torch.zeros(n_local, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)
         s.init(x, G(x), xn)
@@ -342,8 +363,7 @@ def main():
         aa.aa_fill_uniform(dn, nl, -0.9, 0.9, stream_id=1, offset=rank * nl, stream=stream)
         aa.aa_fill_uniform(bn, nl, -1.0, 1.0, stream_id=2, offset=rank * nl, stream=stream)
         Gn = lambda x: torch.addcmul(bn, dn, x)
-        s = aa.AndersonSolver(nl, m, variant, rank=rank, nranks=world, nccl_comm=comm, stream=stream,
-                              n_global=nl * world, fused_allreduce=1 if (args.fused_ar and world > 1) else None)
+        s = make_solver(nl, m, variant)
         x = torch.zeros(nl, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)
         s.init(x, Gn(x), xn)
@@ -423,6 +443,7 @@ def main():
                 "data": "synthetic", "config": _config(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": head["launches"], "clocks": clocks,
                 "detail": {k_: v_ for k_, v_ in head.items() if k_ not in ("launches",)},
+                "global_reduction": ar_mode["mode"],
                 "variants": variants}
         if sweep:
             line["sweep"] = sweep

@@ -85,7 +85,9 @@ enum aa_option {
     AA_OPT_FUSED_ALLREDUCE = 7 /* 1 = every global reduction is a one-shot exchange done by
                                   the producing kernel's last CTA over NVLink peer memory
                                   (CUDA IPC, same node) instead of ncclAllReduce; collective
-                                  (all ranks set it); 0 = ncclAllReduce (default)          */
+                                  (all ranks set it); 0 = ncclAllReduce (default).  If the
+                                  IPC setup fails the call returns its error and the handle
+                                  keeps using ncclAllReduce (not sticky)                    */
 };
 
 /* aa_stats flags */

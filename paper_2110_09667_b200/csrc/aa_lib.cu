@@ -760,28 +760,42 @@ static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant,
 // CUDA IPC handle all-gathered over the handle's NCCL communicator, peers' buffers
 // opened with cudaIpcOpenMemHandle (NVLink P2P within the node).
 static int fused_setup(aa_ctx* c) {
+  // Any failure here leaves the handle usable with ncclAllReduce (not sticky).
   if (c->nranks > MAX_RANKS || !nccl().AllGather) return AA_ERR_ARG;
   const size_t bytes = kFlagBytes + (size_t)2 * c->nranks * LRED * sizeof(double);
-  CUDA_TRY(c, cudaMalloc(&c->xbuf, bytes));
-  CUDA_TRY(c, cudaMemset(c->xbuf, 0, bytes));
-  cudaIpcMemHandle_t mine;
-  CUDA_TRY(c, cudaIpcGetMemHandle(&mine, c->xbuf));
   char* dh = nullptr;
-  CUDA_TRY(c, cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * c->nranks));
-  CUDA_TRY(c, cudaMemcpy(dh + sizeof(mine) * c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice));
-  if (nccl().AllGather(dh + sizeof(mine) * c->rank, dh, sizeof(mine), 0 /*ncclInt8*/, c->comm, c->stream) != 0) {
-    cudaFree(dh);
-    return fail(c, AA_ERR_NCCL);
-  }
   std::vector<cudaIpcMemHandle_t> all(c->nranks);
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  CUDA_TRY(c, cudaMemcpy(all.data(), dh, sizeof(mine) * c->nranks, cudaMemcpyDeviceToHost));
+  cudaIpcMemHandle_t mine;
+  auto undo = [&](int code) {
+    cudaGetLastError();
+    for (int r = 0; r < MAX_RANKS; ++r) {
+      if (c->peer_base[r] && c->peer_base[r] != c->xbuf) cudaIpcCloseMemHandle(c->peer_base[r]);
+      c->peer_base[r] = nullptr;
+    }
+    if (c->xbuf) cudaFree(c->xbuf);
+    if (dh) cudaFree(dh);
+    c->xbuf = nullptr;
+    fprintf(stderr, "libaa: fused NVLink allreduce unavailable (%d); keeping ncclAllReduce\n", code);
+    return code;
+  };
+  if (cudaMalloc(&c->xbuf, bytes) != cudaSuccess || cudaMemset(c->xbuf, 0, bytes) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine, c->xbuf) != cudaSuccess ||
+      cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * c->nranks) != cudaSuccess ||
+      cudaMemcpy(dh + sizeof(mine) * c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice) != cudaSuccess)
+    return undo(AA_ERR_CUDA);
+  if (nccl().AllGather(dh + sizeof(mine) * c->rank, dh, sizeof(mine), 0 /*ncclInt8*/, c->comm, c->stream) != 0)
+    return undo(AA_ERR_NCCL);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess ||
+      cudaMemcpy(all.data(), dh, sizeof(mine) * c->nranks, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return undo(AA_ERR_CUDA);
   cudaFree(dh);
+  dh = nullptr;
   for (int r = 0; r < c->nranks; ++r) {
     if (r == c->rank) {
       c->peer_base[r] = c->xbuf;
-    } else {
-      CUDA_TRY(c, cudaIpcOpenMemHandle(&c->peer_base[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+    } else if (cudaIpcOpenMemHandle(&c->peer_base[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      c->peer_base[r] = nullptr;
+      return undo(AA_ERR_CUDA);
     }
   }
   c->seq = 0;
@@ -831,7 +845,10 @@ int aa_set_option(aa_handle_t h, int opt, double val) {
       return AA_OK;
     case AA_OPT_FUSED_ALLREDUCE:
       if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
-      if (val == 1.0 && h->nranks > 1 && !h->xbuf) RET_IF_(fused_setup(h));
+      if (val == 1.0 && h->nranks > 1 && !h->xbuf) {
+        const int rc = fused_setup(h);   // collective; on failure NCCL stays in use
+        if (rc != AA_OK) return rc;
+      }
       h->fused = (int)val;
       return AA_OK;
     default:
