@@ -313,3 +313,35 @@ def test_reset_restarts_window(config1):
     s.step(x, Gt(x), xn)
     st = s.stats()
     assert st.m_i == 1 and st.logical_last["qradd"] == 1
+
+
+@pytest.mark.parametrize("n", [1, 5, 1000, 4097, 100003])
+def test_no_writes_outside_caller_buffers(n):
+    """Bounds check in lieu of compute-sanitizer (closed on this pool): caller vectors sit
+    inside NaN-filled guard regions; after start-up, recycle, delete and LOO the guards are
+    bitwise untouched and the in-bounds results are finite."""
+    m, pad = 4, 64
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    for v in VARIANTS:
+        bufs = [torch.full((n + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(3)]
+        x, xn, g = (t[pad:pad + n] for t in bufs)
+        x.zero_()
+        s = aa.AndersonSolver(n, m, v, stream=torch.cuda.current_stream())
+        g.copy_(dt * x + bt)
+        s.init(x, g, xn)
+        x, xn = xn, x
+        for _ in range(m + 4):
+            g.copy_(dt * x + bt)
+            s.step(x, g, xn)
+            x, xn = xn, x
+        s.stats(loo=True)
+        s.delete_oldest()
+        g.copy_(dt * x + bt)
+        s.step(x, g, xn)
+        torch.cuda.synchronize()
+        for t in bufs:
+            assert torch.isnan(t[:pad]).all() and torch.isnan(t[pad + n:]).all(), v
+        if not s.stats().breakdown:      # n = 1: every later Delta f is dependent (R_kk = 0)
+            assert torch.isfinite(xn).all()
+        s.close()
