@@ -215,8 +215,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--only-headline", action="store_true")
     ap.add_argument("--icwy-merged", type=int, default=0)
-    ap.add_argument("--workload", default="kernel", choices=("kernel", "em"),
+    ap.add_argument("--workload", default="kernel", choices=("kernel", "em", "heat"),
                     help="kernel: config 2 recycle steps (default); em: PAPER.md §5.3 EM mixture to convergence")
+    ap.add_argument("--grid", type=int, default=8192, help="heat workload: N x N interior grid (config 4: 8192)")
+    ap.add_argument("--term", type=int, default=2, help="heat workload: nonlinear term (P:699 / P:728)")
     ap.add_argument("--fused-ar", type=int, default=1,
                     help="1: one-shot NVLink exchange in the kernel's last CTA instead of ncclAllReduce")
     args = ap.parse_args()
@@ -251,6 +253,8 @@ def main():
 
     if args.workload == "em":
         return run_em(args, torch, dist, rank, world, local_rank)
+    if args.workload == "heat":
+        return run_heat(args, torch, dist, rank, world, local_rank)
 
     uid, comm = None, None
     if world > 1:
@@ -454,6 +458,98 @@ def main():
             line["sweep"] = sweep
         if small_n:
             line["small_n"] = small_n
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_heat(args, torch, dist, rank, world, local_rank):
+    """BASELINE config 4 / PAPER.md §5.1: Picard map of the 2-D heat equation + nonlinear term
+    on an N x N grid (default 8192^2 = 6.7e7 unknowns, term 2, m = 10, tol 1e-8 on ||Delta u||_2),
+    rows split over the ranks; G by exact DST-I (two all-to-all transposes per G on N > 1).
+    Reports iterations and time to solution split into G and AA (CUDA events)."""
+    import math
+    import numpy as np
+    from paper_2110_09667_b200 import aa
+    from aa_inputs import problems as P
+    from aa_inputs.heat_torch import HeatG
+    N, term = args.grid, args.term
+    m = args.m if args.m != 20 else (5 if term == 1 else 10)
+    comm = None
+    if world > 1:
+        dist.barrier()
+        comm = aa.torch_nccl_comm()
+    Nl = N // world
+    stream = torch.cuda.current_stream()
+    # b on the device, this rank's rows (the grid formula is evaluated on the device)
+    h = 1.0 / (N + 1)
+    t = torch.arange(1, N + 1, device="cuda", dtype=torch.float64) * h
+    ty = t[rank * Nl:(rank + 1) * Nl]
+    Y, X = torch.meshgrid(ty, t, indexing="ij")
+    pi = math.pi
+    ue = torch.sin(pi * X) ** 2 * torch.sin(pi * Y) ** 2
+    from aa_inputs.heat_torch import heat_c
+    bvec = (2 * pi ** 2 * (torch.cos(pi * X) ** 2 - torch.sin(pi * X) ** 2) * torch.sin(pi * Y) ** 2
+            + 2 * pi ** 2 * (torch.cos(pi * Y) ** 2 - torch.sin(pi * Y) ** 2) * torch.sin(pi * X) ** 2
+            + heat_c(ue, term)).reshape(-1).contiguous()
+    ue = ue.reshape(-1)
+    del X, Y
+    G = HeatG(N, term, bvec, rank, world, dist)
+    n = Nl * N
+
+    def mx(v):
+        if dist is None:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    res = {}
+    for variant in VARIANTS:
+        s = aa.AndersonSolver(n, m, variant, rank=rank, nranks=world, nccl_comm=comm, stream=stream,
+                              n_global=N * N)
+        if args.fused_ar and world > 1:
+            try:
+                aa.aa_set_option(s.h, aa.OPT_FUSED_ALLREDUCE, 1)
+            except aa.AAError:
+                pass
+        x = torch.zeros(n, dtype=torch.float64, device="cuda")
+        g = torch.empty_like(x)
+        xn = torch.empty_like(x)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        tg = ta = 0.0
+        G(x, g)
+        s.init(x, g, xn)
+        x, xn = xn, x
+        it, conv = 0, False
+        for it in range(1, 301):
+            e[0].record(stream)
+            G(x, g)
+            e[1].record(stream)
+            s.step(x, g, xn)
+            e[2].record(stream)
+            st = s.stats()
+            tg += e[0].elapsed_time(e[1])
+            ta += e[1].elapsed_time(e[2])
+            x, xn = xn, x
+            if st.dx_norm < 1e-8:
+                conv = True
+                break
+        err = (x - ue).abs().max()
+        if dist is not None:
+            dist.all_reduce(err, op=dist.ReduceOp.MAX)
+        s.close()
+        res[variant] = {"iterations": it, "converged": conv, "G_ms": mx(tg), "AA_ms": mx(ta),
+                        "us_per_AA_iter": mx(ta) * 1e3 / max(it, 1), "max_err_vs_u_exact": float(err)}
+    if rank == 0:
+        line = {"metric": "Heat 2D + nonlinear term (PAPER.md §5.1, BASELINE config 4): AA time to solution, µs per AA iteration",
+                "value": res["icwy"]["us_per_AA_iter"], "unit": "us/iter", "n_gpus": world,
+                "higher_is_better": False, "scaling": "strong", "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "heat_picard", "grid": N, "n_global": N * N, "term": term, "m": m,
+                           "tol": "||Delta u||_2 < 1e-8", "G": "exact DST-I solve (reading A19)"},
+                "variants": res}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
