@@ -25,10 +25,15 @@ def laplacian_eigs(N: int, device, dtype=torch.float64) -> torch.Tensor:
     return -(4.0 / h ** 2) * (s[:, None] + s[None, :])
 
 
+BRATU_LAMBDA = 6.7
+
+
 def heat_c(u: torch.Tensor, term: int) -> torch.Tensor:
     if term == 1:
         e = torch.exp(u)
         return u + u * e + u / e + (u - e) ** 2
+    if term == 3:   # Bratu (§5.2): A u + lambda e^u = 0
+        return BRATU_LAMBDA * torch.exp(u)
     return 100.0 * (u - u * u)
 
 

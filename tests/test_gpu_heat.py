@@ -30,10 +30,10 @@ def test_torch_dst_matches_scipy():
     assert np.allclose(G(torch.tensor(u, device="cuda")).cpu().numpy(), P.heat_G(u, N, 2, b), rtol=1e-12, atol=1e-14)
 
 
-def _gpu_solve(N, term, m, variant, tol, maxit):
+def _gpu_solve(N, term, m, variant, tol, maxit, **opts):
     b = torch.tensor(P.heat_rhs(N, term), device="cuda")
     G = HeatG(N, term, b)
-    s = aa.AndersonSolver(N * N, m, variant, stream=torch.cuda.current_stream())
+    s = aa.AndersonSolver(N * N, m, variant, stream=torch.cuda.current_stream(), **opts)
     x = torch.zeros(N * N, dtype=torch.float64, device="cuda")
     xn = torch.empty_like(x)
     s.init(x, G(x), xn)
@@ -71,3 +71,23 @@ def test_heat_term2_dcgs2_reported_not_failed():
     [Pr8]); the GPU run must simply complete without error."""
     it, u = _gpu_solve(128, 2, 10, "dcgs2", 1e-8, 60)
     assert u.shape == (128 * 128,)
+
+
+@pytest.mark.parametrize("variant,opts,okw", [("mgs", {}, {}), ("icwy", {}, {}), ("cgs2", {}, {}),
+                                              ("dcgs2", {"dcgs2_rscale": 1}, {"dcgs2_rscale": True})])
+def test_bratu_envelope(variant, opts, okw):
+    """Bratu (§5.2): lambda = 6.7, m = 30, tol 1e-10, 128^2."""
+    N, tol = 128, 1e-10
+    b = P.heat_rhs(N, 3)
+    G = lambda u: P.heat_G(u, N, 3, b)
+    env, sols = [], []
+    for p in (1, 2, 3, 7):
+        r = aa_variant(G, np.zeros(N * N), 30, variant, 100, tol=tol, shards=p, record_x=False,
+                       record_loo=False, **okw)
+        if r.converged:
+            env.append(r.iters)
+            sols.append(r.x)
+    assert env and max(env) < 30
+    it, u = _gpu_solve(N, 3, 30, variant, tol, 100, **opts)
+    assert it is not None and min(env) - 2 <= it <= max(env) + 2, (it, env)
+    assert min(np.linalg.norm(u - s_) for s_ in sols) <= 1e3 * tol

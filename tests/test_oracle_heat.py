@@ -69,3 +69,22 @@ def test_term1_and_term2_bands():
             assert counts[v] is not None and lo <= counts[v] <= hi, (term, counts)
         if term == 1:
             assert counts["dcgs2"] is not None and lo <= counts["dcgs2"] <= hi
+
+
+def test_bratu_band_and_dcgs2_readings():
+    """Bratu (§5.2, lambda = 6.7, m = 30, tol 1e-10): every variant converges in
+    < 30 iterations -- DCGS-2 only with the consistent R update of reading A3
+    (R += R_kk s); the verbatim Alg. 6 l.5 (R += s) diverges on this problem and on heat
+    term 2, contradicting the paper's reported results (reading A3)."""
+    N = 64
+    b = P.heat_rhs(N, 3)
+    G = lambda u: P.heat_G(u, N, 3, b)
+    for v in ("mgs", "icwy", "cgs2"):
+        r = aa_variant(G, np.zeros(N * N), 30, v, 100, tol=1e-10, record_x=False, record_loo=False)
+        assert r.converged and r.iters < 30
+    r = aa_variant(G, np.zeros(N * N), 30, "dcgs2", 100, tol=1e-10, dcgs2_rscale=True,
+                   record_x=False, record_loo=False)
+    assert r.converged and r.iters < 30
+    with np.errstate(all="ignore"):
+        r = aa_variant(G, np.zeros(N * N), 30, "dcgs2", 60, tol=1e-10, record_x=False, record_loo=False)
+    assert not r.converged
