@@ -205,6 +205,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--m", type=int, default=20)
     ap.add_argument("--n-local", type=float, default=1e8)
+    ap.add_argument("--n-global", type=float, default=0,
+                    help="strong scaling (config 3: 4e8): n_local = n_global / N instead of --n-local")
     ap.add_argument("--variant", default="dcgs2", choices=VARIANTS)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--ref-n", type=float, default=1e6)
@@ -261,7 +263,11 @@ def main():
         dist.barrier()
         comm = aa.torch_nccl_comm()   # libaa borrows the process group's NCCL communicator
 
-    n_local = int(args.n_local)
+    if args.n_global:
+        n_local = int(args.n_global) // world          # config 3: fixed global size
+        args.n_local = n_local
+    else:
+        n_local = int(args.n_local)
     offset = rank * n_local
     stream = torch.cuda.current_stream()
     d = torch.empty(n_local, dtype=torch.float64, device="cuda")
@@ -448,7 +454,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": head["ms_per_step"] * 1e3, "unit": "us/iter", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
-                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": False, "scaling": "strong" if args.n_global else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": _config(args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": head["launches"], "clocks": clocks,
                 "detail": {k_: v_ for k_, v_ in head.items() if k_ not in ("launches",)},

@@ -1,0 +1,104 @@
+"""BASELINE config 5 (orthogonality stress) at full size: n = 1e7, m = 50.
+
+5a: A = U Sigma V^T with sigma_j = 1e-12^(j/49) (kappa = 1e12) appended column by column with
+    aa_test_qradd; LOO ||I - Q^T Q||_F and ||A - QR||/||A|| against the oracle's (same
+    columns, same variant).  SURVEY [Pr5] classes: MGS/ICWY ~ eps kappa, CGS-2 ~ eps,
+    DCGS-2 up to O(1).
+5b: AA on G = d*x + b with d ~ U[0.5, 0.99) (windows driven to cond ~1e15, [Pr7]),
+    tol 1e-10; block-constant over 1e4 blocks so the 1e4-row oracle is exact; iteration count
+    within the oracle's summation-order envelope, max LOO comparable.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from aa_inputs import problems  # noqa: E402
+from oracle import EPS, Ledger, QRState, Reducer, aa_variant, loss_of_orthogonality, qradd  # noqa: E402
+from paper_2110_09667_b200 import aa  # noqa: E402
+
+N5, M5 = 10_000_000, 50
+
+
+@pytest.fixture(scope="module")
+def stress_matrix():
+    return problems.ortho_test_matrix(N5, M5, 1e12, seed=5)
+
+
+@pytest.mark.parametrize("variant", ["mgs", "icwy", "cgs2", "dcgs2"])
+def test_config5a_full_size(stress_matrix, variant):
+    A = stress_matrix
+    st, led, red = QRState(N5, M5), Ledger(), Reducer(1)
+    r0 = red.norm(A[:, 0]); st.R[0, 0] = r0; st.Q[:, 0] = A[:, 0] / r0; st.mi = 1
+    for j in range(1, M5):
+        qradd(variant, st, A[:, j], led, red)
+    loo_o = loss_of_orthogonality(st.Q)
+    s = aa.AndersonSolver(N5, M5, variant, stream=torch.cuda.current_stream(), breakdown_eps=0.0)
+    z = torch.zeros(N5, dtype=torch.float64, device="cuda")
+    x1 = torch.empty_like(z)
+    s.init(z, z, x1)
+    col = torch.empty(N5, dtype=torch.float64, device="cuda")
+    for j in range(M5):
+        col.copy_(torch.from_numpy(np.ascontiguousarray(A[:, j])))
+        aa.aa_test_qradd(s.h, col)
+    loo_g = s.stats(loo=True).loo
+    R, _, _, _ = aa.aa_get_small(s.h, M5, M5)
+    q = torch.empty(N5 * M5, dtype=torch.float64, device="cuda")
+    aa.aa_get_q(s.h, q)
+    Qg = q.view(M5, N5)
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).to("cuda")
+    resid = torch.linalg.norm(At - torch.tensor(R.T, device="cuda") @ Qg) / torch.linalg.norm(At)
+    resid_o = np.linalg.norm(A - st.Q @ st.R) / np.linalg.norm(A)
+    s.close()
+    floor = 10 * M5 * EPS * np.sqrt(N5 / 4736)
+    if variant == "dcgs2":
+        # O(eps) kappa^2 regime: complete loss of orthogonality is the expected class ([Pr5])
+        assert loo_g <= 10 * max(loo_o, 1.0)
+    else:
+        assert loo_g <= max(10 * loo_o, floor), (loo_g, loo_o)
+    if variant == "cgs2":
+        assert loo_g < 1e-12
+    if variant in ("mgs", "icwy"):
+        assert loo_g > 1e3 * floor / 10          # really the eps*kappa class, not CGS-2's
+    assert float(resid) <= max(10 * resid_o, 1e-12), (float(resid), resid_o)
+
+
+@pytest.mark.parametrize("variant", ["mgs", "icwy", "cgs2", "dcgs2"])
+def test_config5b_aa_run(variant):
+    P5 = 10_000
+    W = N5 // P5
+    w, d, b = problems.block_constant(N5, P5, 0.5, 0.99)
+    # windows reach cond ~1e15 here, where the eps*kappa classes are chaotic: summation order
+    # alone moves ICWY's max LOO from 0.04 to 0.8 -> compare with the summation-order envelope
+    env, loos = [], []
+    for p in (1, 2, 3, 7):
+        r = aa_variant(lambda x: d * x + b, np.zeros(P5), M5, variant, 500, tol=1e-10, shards=p,
+                       record_x=False, record_loo=True)
+        if r.converged:
+            env.append(r.iters)
+        loos.append(max(r.loo))
+    dt = torch.tensor(d, device="cuda").repeat_interleave(W)
+    bt = torch.tensor(b, device="cuda").repeat_interleave(W)
+    s = aa.AndersonSolver(N5, M5, variant, stream=torch.cuda.current_stream(), breakdown_eps=0.0)
+    x = torch.zeros(N5, dtype=torch.float64, device="cuda")
+    xn = torch.empty_like(x)
+    s.init(x, torch.addcmul(bt, dt, x), xn)
+    x, xn = xn, x
+    it, conv, loo_max = 0, False, 0.0
+    for it in range(1, 501):
+        s.step(x, torch.addcmul(bt, dt, x), xn)
+        x, xn = xn, x
+        st = s.stats(loo=(it % 10 == 0))
+        if it % 10 == 0:
+            loo_max = max(loo_max, st.loo)
+        if st.dx_norm < 1e-10 * np.sqrt(W):     # same per-block tolerance as the 1e4-row oracle
+            conv = True
+            break
+    s.close()
+    assert conv and env
+    assert min(env) - 3 <= it <= max(env) + 3, (it, env)
+    assert loo_max <= max(10 * max(loos), 10 * M5 * EPS * np.sqrt(N5 / 4736))
