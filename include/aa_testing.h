@@ -41,6 +41,14 @@ int64_t aa_kernel_launches(aa_handle_t h);
 int aa_fill_uniform(double* out_dev, int64_t n, int64_t offset, uint64_t seed, uint64_t stream,
                     double lo, double hi, void* cuda_stream);
 
+/* Test-only phase timeline: enable = 1 allocates a 384-word device buffer; every kernel's
+ * CTA 0 (slots op*16 + 0..5, K4 head sub-phases 8..11) and last CTA (slots 6, 7) record
+ * %globaltimer (ns) at: entry, after staging, after the head, first tile ready, tiles done,
+ * partials written, reduction begin, end; words 128 + slot hold clock64 at the same points;
+ * words 256.. hold clock64 at each Givens step of K4's QRDelete precompute.
+ * out384 (host, may be NULL) receives the buffer (synchronises). */
+int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384);
+
 /* Build-time facts: sm target, tile rows, stages, block size (for the report). */
 int aa_build_info(char* buf, int len);
 

@@ -26,7 +26,7 @@ PHASES = ("qradd", "qrdelete", "lsp_rhs", "norm_check", "other")
 EXPORTS = ("aa_comm_unique_id", "aa_create", "aa_create_with_comm", "aa_set_option", "aa_init", "aa_step", "aa_step_host",
            "aa_delete_oldest", "aa_stats", "aa_reset", "aa_destroy", "aa_status_string",
            "aa_test_qradd", "aa_get_small", "aa_get_q", "aa_timings", "aa_kernel_launches",
-           "aa_fill_uniform", "aa_build_info")
+           "aa_fill_uniform", "aa_build_info", "aa_test_timeline")
 
 
 class AAStatsC(C.Structure):
@@ -62,6 +62,7 @@ def _load():
         "aa_kernel_launches": (i64, [vp]),
         "aa_fill_uniform": (i32, [vp, i64, i64, C.c_uint64, C.c_uint64, dbl, dbl, vp]),
         "aa_build_info": (i32, [C.c_char_p, i32]),
+        "aa_test_timeline": (i32, [vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -234,6 +235,20 @@ def aa_fill_uniform(out, n: int, lo: float, hi: float, *, stream_id: int, seed: 
                     offset: int = 0, stream=None) -> None:
     _chk(_lib.aa_fill_uniform(_ptr(out), n, offset, seed, stream_id, lo, hi, _stream_ptr(stream)),
          "aa_fill_uniform")
+
+
+def aa_test_timeline(h: int, enable: bool = True):
+    import numpy as np
+    out = np.zeros(384, dtype=np.uint64)
+    _chk(_lib.aa_test_timeline(h, 1 if enable else 0, out.ctypes.data), "aa_test_timeline")
+    return out[:256].reshape(2, 8, 16)
+
+
+def aa_test_timeline_raw(h: int):
+    import numpy as np
+    out = np.zeros(384, dtype=np.uint64)
+    _chk(_lib.aa_test_timeline(h, 1, out.ctypes.data), "aa_test_timeline")
+    return out
 
 
 def aa_build_info() -> str:

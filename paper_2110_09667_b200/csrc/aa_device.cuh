@@ -109,6 +109,8 @@ struct alignas(64) KParams {
   int final_slot;   // reduction slot holding (||v'||^2, v'^T f)
   int red_slot;     // slot this kernel writes
   int words;        // words this kernel reduces
+  int red_words0;   // words of reduction slot 0 the heads stage into shared memory
+  unsigned long long* tl;   // test-only phase timeline (CTA 0 / last CTA, %globaltimer ns), or null
   int nin, tr, stages;
   int vb;           // first vector column (= sum of block columns)
   int tm3d;         // column blocks use 3-D maps (TR a multiple of 256)
@@ -211,19 +213,30 @@ __device__ __forceinline__ double warp_sum(double v) {
 // in shared memory, leading dimension MMAX, and end with __syncwarp().
 
 // QRDelete on R (reading A7): drop column 0 of the mold x mold
-// factor, re-triangularise the upper-Hessenberg remainder with mold-1 Givens
-// rotations of adjacent rows, rho = hypot(a,b) >= 0.  Output Rw ((mold-1)^2, col-major
-// MMAX) and the rotation coefficients cs/sn (applied to Q's columns by K1).
-__device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double* cs, double* sn) {
+// factor, re-triangularise the upper-Hessenberg remainder H = R[:, 1:] with mold-1 Givens
+// rotations of adjacent rows, rho = hypot(a,b) >= 0.  Output Rw ((mold-1)^2 upper
+// triangular, zeros below, col-major MMAX) and the rotation coefficients cs/sn (applied to
+// Q's columns by K1).
+// Register form: lane l owns Hessenberg columns l and l+32; "carry" is the column's entry
+// in the row being rotated (row j at step j), row j+1 is still the original R and is
+// prefetched one step ahead, so the serial chain per step is one shuffle, the hypot and
+// two products (no shared-memory round trip, no __syncwarp).
+__device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double* cs, double* sn,
+                                 unsigned long long* tsteps = nullptr) {
   const int lane = threadIdx.x & 31;
   const int nc = mold - 1;  // columns of the Hessenberg matrix
-  for (int idx = lane; idx < mold * nc; idx += 32) {
-    int i = idx % mold, j = idx / mold;
-    Rw[i + j * MMAX] = (i <= j + 1) ? Rg[i + (j + 1) * MMAX] : 0.0;
-  }
-  __syncwarp();
+  const int l0 = lane, l1 = lane + 32;
+  // H[i][l] = Rg[i + (l+1) MMAX] for i <= l+1 (R upper triangular), else 0
+  auto h = [&](int i, int l) -> double { return (l < nc && i <= l + 1) ? Rg[i + (l + 1) * MMAX] : 0.0; };
+  double carry0 = h(0, l0), carry1 = h(0, l1);
+  double h20 = h(1, l0), h21 = h(1, l1);
+  double bn = (nc > 0) ? Rg[1 + 1 * MMAX] : 0.0;
   for (int j = 0; j < nc; ++j) {
-    const double a = Rw[j + j * MMAX], b = Rw[j + 1 + j * MMAX];
+    if (tsteps && lane == 0) tsteps[j] = clock64();
+    const double b = bn;                        // H[j+1][j], original
+    const double n20 = h(j + 2, l0), n21 = h(j + 2, l1);   // next step's row j+2
+    bn = (j + 1 < nc) ? Rg[(j + 2) + (j + 2) * MMAX] : 0.0;
+    const double a = __shfl_sync(0xffffffffu, j < 32 ? carry0 : carry1, j & 31);
     // rho = hypot(a, b) >= 0; the plain form is exact to rounding unless a^2 + b^2 would
     // over/underflow, where hypot's scaling takes over.  One reciprocal, two products.
     const double aa = fabs(a), bb = fabs(b), mx = fmax(aa, bb);
@@ -231,48 +244,73 @@ __device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double*
     const double ri = rho > 0.0 ? 1.0 / rho : 0.0;
     const double c = rho > 0.0 ? a * ri : 1.0;
     const double s = rho > 0.0 ? b * ri : 0.0;
-    for (int l = j + 1 + lane; l < nc; l += 32) {
-      const double h1 = Rw[j + l * MMAX], h2 = Rw[j + 1 + l * MMAX];
-      Rw[j + l * MMAX] = __dadd_rn(__dmul_rn(c, h1), __dmul_rn(s, h2));
-      Rw[j + 1 + l * MMAX] = __dadd_rn(__dmul_rn(-s, h1), __dmul_rn(c, h2));
+    if (l0 > j && l0 < nc) {
+      Rw[j + l0 * MMAX] = __dadd_rn(__dmul_rn(c, carry0), __dmul_rn(s, h20));
+      carry0 = __dadd_rn(__dmul_rn(-s, carry0), __dmul_rn(c, h20));
     }
-    __syncwarp();
+    if (l1 > j && l1 < nc) {
+      Rw[j + l1 * MMAX] = __dadd_rn(__dmul_rn(c, carry1), __dmul_rn(s, h21));
+      carry1 = __dadd_rn(__dmul_rn(-s, carry1), __dmul_rn(c, h21));
+    }
+    for (int i = j + 1 + lane; i < mold; i += 32) Rw[i + j * MMAX] = 0.0;   // column j below rho
     if (lane == 0) {
       Rw[j + j * MMAX] = rho;
-      Rw[j + 1 + j * MMAX] = 0.0;
       cs[j] = c;
       sn[j] = s;
     }
-    __syncwarp();
-  }
-}
-
-// Forward substitution with a unit lower-triangular T (Alg. 4 l.4 "T^{-1} R"; A5):
-// r <- T^{-1} r in place, r has k entries in shared memory.
-__device__ void k3_forward_unit_lower(const double* T, double* r, int k) {
-  const int lane = threadIdx.x & 31;
-  for (int l = 0; l < k; ++l) {
-    __syncwarp();
-    const double rl = r[l];
-    for (int j = l + 1 + lane; j < k; j += 32) r[j] -= T[j + l * MMAX] * rl;
+    h20 = n20;
+    h21 = n21;
   }
   __syncwarp();
 }
 
+// Forward substitution with a unit lower-triangular T (Alg. 4 l.4 "T^{-1} R"; A5):
+// r <- T^{-1} r in place, r has k entries in shared memory.  Lane j holds r_j (and
+// r_{j+32}); step l broadcasts r_l with one shuffle; T's column l+1 is prefetched.
+__device__ void k3_forward_unit_lower(const double* T, double* r, int k) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = lane, j1 = lane + 32;
+  double r0 = (j0 < k) ? r[j0] : 0.0, r1 = (j1 < k) ? r[j1] : 0.0;
+  double t0 = (j0 < k && k > 0) ? T[j0] : 0.0, t1 = (j1 < k && k > 0) ? T[j1] : 0.0;
+  for (int l = 0; l < k; ++l) {
+    const double tn0 = (j0 < k && l + 1 < k) ? T[j0 + (l + 1) * MMAX] : 0.0;
+    const double tn1 = (j1 < k && l + 1 < k) ? T[j1 + (l + 1) * MMAX] : 0.0;
+    const double rl = __shfl_sync(0xffffffffu, l < 32 ? r0 : r1, l & 31);
+    if (j0 > l && j0 < k) r0 -= t0 * rl;
+    if (j1 > l && j1 < k) r1 -= t1 * rl;
+    t0 = tn0;
+    t1 = tn1;
+  }
+  if (j0 < k) r[j0] = r0;
+  if (j1 < k) r[j1] = r1;
+  __syncwarp();
+}
+
 // Back substitution R gamma = c (Alg. 2 l.9), R upper triangular K x K; c overwritten.
+// Lane i holds c_i (and c_{i+32}) and 1/R_ii; step j: lane j forms gamma_j, one shuffle
+// broadcasts it, every lane updates its c_i with R's column j (prefetched a step ahead).
 __device__ void k3_back_subst(const double* R, double* c, double* gamma, int K) {
   const int lane = threadIdx.x & 31;
+  const int i0 = lane, i1 = lane + 32;
+  double c0 = (i0 < K) ? c[i0] : 0.0, c1 = (i1 < K) ? c[i1] : 0.0;
   // reciprocals of the diagonal in parallel, so the serial chain has no division
-  double rinv0 = 0.0, rinv1 = 0.0;
-  if (lane < K) rinv0 = 1.0 / R[lane + lane * MMAX];
-  if (lane + 32 < K) rinv1 = 1.0 / R[(lane + 32) + (lane + 32) * MMAX];
+  const double rinv0 = (i0 < K) ? 1.0 / R[i0 + i0 * MMAX] : 0.0;
+  const double rinv1 = (i1 < K) ? 1.0 / R[i1 + i1 * MMAX] : 0.0;
+  double r0 = (i0 < K && K > 0) ? R[i0 + (K - 1) * MMAX] : 0.0;
+  double r1 = (i1 < K && K > 0) ? R[i1 + (K - 1) * MMAX] : 0.0;
   for (int j = K - 1; j >= 0; --j) {
-    __syncwarp();
-    const double rj = __shfl_sync(0xffffffffu, j < 32 ? rinv0 : rinv1, j & 31);
-    const double gj = c[j] * rj;
+    const double rn0 = (i0 < j && j >= 1) ? R[i0 + (j - 1) * MMAX] : 0.0;
+    const double rn1 = (i1 < j && j >= 1) ? R[i1 + (j - 1) * MMAX] : 0.0;
+    const double mine = (j < 32) ? c0 * rinv0 : c1 * rinv1;
+    const double gj = __shfl_sync(0xffffffffu, mine, j & 31);
     if (lane == 0) gamma[j] = gj;
-    for (int i = lane; i < j; i += 32) c[i] -= R[i + j * MMAX] * gj;
+    if (i0 < j) c0 -= r0 * gj;
+    if (i1 < j) c1 -= r1 * gj;
+    r0 = rn0;
+    r1 = rn1;
   }
+  if (i0 < K) c[i0] = c0;
+  if (i1 < K) c[i1] = c1;
   __syncwarp();
 }
 

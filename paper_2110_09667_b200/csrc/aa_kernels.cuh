@@ -28,6 +28,17 @@ namespace aa {
 
 constexpr int MAXSTAGES = 8;
 
+// test-only phase timeline: slot s of the op's 16-slot row gets %globaltimer
+#define AA_TL(s)                                                                                   \
+  do {                                                                                             \
+    if (p.tl && threadIdx.x == 0) {                                                                \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      p.tl[OP * 16 + (s)] = t_;                                                                    \
+      p.tl[128 + OP * 16 + (s)] = (unsigned long long)clock64();                                   \
+    }                                                                                              \
+  } while (0)
+
 struct HeadArea {
   double coef[NIN_MAX];
   double coef2[MMAX + 2];
@@ -46,7 +57,11 @@ __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + 
 __host__ __device__ constexpr size_t head_bytes() { return align_up(sizeof(HeadArea), 128); }
 __host__ __device__ constexpr size_t bar_bytes() { return 128; }
 // scratch for the head / commit (aliases the stage ring before and after the pipeline)
-__host__ __device__ constexpr size_t scratch_bytes() { return (2 * MMAX * MMAX + 4 * MMAX) * sizeof(double); }
+// scratch (aliases the stage ring before / after the pipeline):
+// [Rw MMAX^2][Tw MMAX^2][v1, cvec, cvec2, spare: 4 x MMAX][R0: copy of reduction slot 0][RF: 8 words]
+constexpr size_t SCR_R0 = 2 * MMAX * MMAX + 4 * MMAX;
+constexpr size_t SCR_RF = SCR_R0 + LRED;
+__host__ __device__ constexpr size_t scratch_bytes() { return (SCR_RF + 8) * sizeof(double); }
 
 __device__ __forceinline__ double cur_scale(const KParams& p, int j) {
   // scale of stored Q column j as seen after this step's K1: rotated columns (QRDelete)
@@ -55,23 +70,44 @@ __device__ __forceinline__ double cur_scale(const KParams& p, int j) {
 }
 
 // ---------------------------------------------------------------------------- heads
-// Assemble ICWY's T' (k x k unit lower) into Tw: rows 0..k-2 from the stored T
-// (start-up) or the post-delete Gram (recycle / delete-only), row k-1 from Alg. 4 l.1.
-__device__ void icwy_assemble_T(const KParams& p, const double* red0, double* Tw, int k) {
-  const int lane = threadIdx.x & 31;
-  const K1Layout L = K1Layout::make(k, true, p.gram != 0);
-  for (int idx = lane; idx < k * k; idx += 32) {
-    const int i = idx % k, j = idx / k;
-    double v;
-    if (i == j) v = 1.0;
-    else if (j > i) v = 0.0;
-    else if (p.flags & F_DELETE_ONLY) v = red0[i * (i - 1) / 2 + j];
-    else if (i == k - 1) v = red0[L.off_x + j];
-    else if (p.recycle) v = red0[L.off_gram + i * (i - 1) / 2 + j];
-    else v = p.st->f[p.ver].T[i + j * MMAX];
-    Tw[i + j * MMAX] = v;
+// All threads: copy what the head's serial K3 math reads into shared memory in one round
+// of parallel loads (columns per warp, no index divisions): reduction slot 0 (R0), the final
+// reduction words (RF), R or QRDelete(R) (Rw, K4), and ICWY's T' (Tw: rows 0..k-2 from the
+// stored T (start-up) or the post-delete Gram (recycle / delete-only), row k-1 from Alg. 4
+// l.1, unit diagonal).
+template <int OP>
+__device__ void stage_small(const KParams& p, double* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = p.k;
+  double* Rw = scratch;
+  double* Tw = scratch + MMAX * MMAX;
+  double* R0 = scratch + SCR_R0;
+  double* RF = scratch + SCR_RF;
+  const int nw = (OP == OP_K4 || OP == OP_K2_ICWY) ? p.red_words0 : 0;
+  for (int w = tid; w < nw; w += NT) R0[w] = p.red[w];
+  if (tid < 2) RF[tid] = p.red[(size_t)p.final_slot * LRED + tid];
+  const Factors& F = p.st->f[p.ver];
+  if constexpr (OP == OP_K4) {
+    const double* Rsrc = p.recycle ? F.Rdel : F.R;
+    for (int j = warp; j < k; j += NWARP)
+      for (int i = lane; i < k; i += 32) Rw[i + j * MMAX] = Rsrc[i + j * MMAX];
   }
-  __syncwarp();
+  if (p.variant == V_ICWY && (OP == OP_K4 || OP == OP_K2_ICWY)) {
+    __syncthreads();   // R0 complete
+    const K1Layout L = K1Layout::make(k, true, p.gram != 0);
+    const bool del_only = p.flags & F_DELETE_ONLY;
+    for (int j = warp; j < k; j += NWARP)
+      for (int i = lane; i < k; i += 32) {
+        double v;
+        if (i == j) v = 1.0;
+        else if (j > i) v = 0.0;
+        else if (del_only) v = R0[i * (i - 1) / 2 + j];
+        else if (i == k - 1) v = R0[L.off_x + j];
+        else if (p.recycle) v = R0[L.off_gram + i * (i - 1) / 2 + j];
+        else v = F.T[i + j * MMAX];
+        Tw[i + j * MMAX] = v;
+      }
+  }
 }
 
 struct K4Head {
@@ -84,35 +120,25 @@ struct K4Head {
 // back-substitution.  Writes Rw (K x K), Tw (ICWY), gamma into H.coef, c into cvec.
 __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   const int lane = threadIdx.x & 31;
-  double* Rw = scratch;
-  double* Tw = scratch + MMAX * MMAX;
-  double* v1 = Tw + MMAX * MMAX;  // MMAX words
-  double* cvec = v1 + MMAX;       // MMAX
-  double* cvec2 = cvec + MMAX;    // MMAX
-  const double* red0 = p.red;
+  double* Rw = scratch;                 // R' (staged by stage_small)
+  double* Tw = scratch + MMAX * MMAX;   // ICWY T' (staged)
+  double* v1 = Tw + MMAX * MMAX;        // MMAX words
+  double* cvec = v1 + MMAX;             // MMAX
+  double* cvec2 = cvec + MMAX;          // MMAX
+  const double* red0 = scratch + SCR_R0;
+  const double* fin = scratch + SCR_RF;
   const int k = p.k;
   K4Head out{};
-  const Factors& F = p.st->f[p.ver];
-  // R' = QRDelete(R) precomputed with this version (recycle), else R itself
-  const double* Rsrc = p.recycle ? F.Rdel : F.R;
-  for (int idx = lane; idx < k * k; idx += 32) {
-    const int i = idx % k, j = idx / k;
-    Rw[i + j * MMAX] = Rsrc[i + j * MMAX];
-  }
-  __syncwarp();
   if (p.flags & F_DELETE_ONLY) {
-    if (p.variant == V_ICWY) icwy_assemble_T(p, red0, Tw, k);
     out.K = k;
     return out;
   }
   const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
-  const double* fin = p.red + p.final_slot * LRED;
   const double vv = (k == 0) ? red0[1] : fin[0];
   const double vf = (k == 0) ? red0[3] : fin[1];
   const double rkk = sqrt(vv);
   // new R column (rows 0..k-1 of column k)
   if (p.variant == V_ICWY && k >= 1) {
-    icwy_assemble_T(p, red0, Tw, k);
     for (int j = lane; j < k; j += 32) v1[j] = red0[L.off_df + j];
     __syncwarp();
     k3_forward_unit_lower(Tw, v1, k);
@@ -134,17 +160,16 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
       Rw[j + (k - 1) * MMAX] += p.rscale ? rk1 * s : s;
     }
   }
-  if (lane == 0) {
-    Rw[k + k * MMAX] = rkk;
-    for (int i = 0; i < k; ++i) Rw[k + i * MMAX] = 0.0;
-  }
+  if (lane == 0) Rw[k + k * MMAX] = rkk;
+  for (int i = lane; i < k; i += 32) Rw[k + i * MMAX] = 0.0;
   // c = Q^T f_i with the final Q
   for (int j = lane; j < k; j += 32) cvec[j] = red0[L.off_f + j];
   __syncwarp();
-  if (p.variant == V_DCGS2 && p.reortho && lane == 0) {
-    double acc = cvec[k - 1];
-    for (int j = 0; j < k - 1; ++j) acc -= red0[L.off_x + j] * cvec[j];
-    cvec[k - 1] = acc;
+  if (p.variant == V_DCGS2 && p.reortho) {
+    double acc = 0.0;
+    for (int j = lane; j < k - 1; j += 32) acc += red0[L.off_x + j] * cvec[j];
+    acc = warp_sum(acc);
+    if (lane == 0) cvec[k - 1] -= acc;
   }
   if (lane == 0) cvec[k] = vf / rkk;
   __syncwarp();
@@ -182,27 +207,30 @@ __device__ K4Head k4_scalars_head(const KParams& p) {
 }
 
 // CTA 0 of K4 (warp 0): write factor version ver^1 from the head's results in shared
-// memory (Rw, Tw in scratch; gamma in H.coef).
-__device__ void k4_write_next(const KParams& p, HeadArea& H, const double* scratch, const K4Head& hd) {
+// memory (Rw = R_new, Tw = T'; gamma in H.coef), then precompute QRDelete(R_new) for the
+// next step from the same shared copy (Givens work area: Tw, after T' is
+// written), so the next recycle step's heads only load it.
+__device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, const K4Head& hd) {
+  constexpr int OP = OP_K4;
   const int lane = threadIdx.x & 31;
-  const double* Rw = scratch;
-  const double* Tw = scratch + MMAX * MMAX;
+  double* Rw = scratch;
+  double* Tw = scratch + MMAX * MMAX;
   const Factors& Fi = p.st->f[p.ver];
   Factors& Fo = p.st->f[p.ver ^ 1];
   const int K = hd.K;
-  const bool del_only = p.flags & F_DELETE_ONLY;
   const int mm = p.m;
-  for (int idx = lane; idx < mm * mm; idx += 32) {
-    const int i = idx % mm, j = idx / mm;
-    Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * MMAX] : 0.0;
-    if (p.variant == V_ICWY) {
-      double v = 0.0;
-      if (i == j) v = (i < K) ? 1.0 : 0.0;
-      else if (j < i && i < p.k) v = Tw[i + j * MMAX];
-      Fo.T[i + j * MMAX] = v;
+  const bool del_only = p.flags & F_DELETE_ONLY;
+  for (int j = 0; j < mm; ++j)
+    for (int i = lane; i < mm; i += 32) {
+      Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * MMAX] : 0.0;
+      if (p.variant == V_ICWY) {
+        double v = 0.0;
+        if (i == j) v = (i < K) ? 1.0 : 0.0;
+        else if (j < i && i < p.k) v = Tw[i + j * MMAX];
+        Fo.T[i + j * MMAX] = v;
+      }
     }
-  }
-  for (int j = lane; j < p.m; j += 32) {
+  for (int j = lane; j < mm; j += 32) {
     double s = Fi.scale[j];
     if (p.recycle && j < p.k) s = 1.0;
     if (!del_only) {
@@ -213,30 +241,19 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, const double* scrat
     Fo.scale[j] = s;
     Fo.gamma[j] = del_only ? 0.0 : ((j < K) ? H.coef[j] : 0.0);
   }
-  if (lane == 0) {
-    Fo.K = K;
-    Fo.has_del = 0;
-  }
+  if (lane == 0) Fo.K = K;
   __syncwarp();
-}
-
-// CTA 0 of K4 (warp 0), after its tiles: QRDelete of the new R, stored
-// with the version so the next recycle step's heads only load it.
-__device__ void k4_precompute_delete(const KParams& p, double* scratch) {
-  const int lane = threadIdx.x & 31;
-  Factors& Fo = p.st->f[p.ver ^ 1];
-  __threadfence_block();
-  const int K = Fo.K;
+  AA_TL(9);
+  // QRDelete of the new R, from shared memory
   if (K >= 1) {
-    k3_givens_delete(Fo.R, K, scratch, Fo.cs, Fo.sn);
-    const int mm = p.m;
-    for (int idx = lane; idx < mm * mm; idx += 32) {
-      const int i = idx % mm, j = idx / mm;
-      Fo.Rdel[i + j * MMAX] = (i < K - 1 && j < K - 1) ? scratch[i + j * MMAX] : 0.0;
-    }
+    k3_givens_delete(Rw, K, Tw, Fo.cs, Fo.sn, p.tl ? p.tl + 256 : nullptr);
+    AA_TL(10);
+    for (int j = 0; j < mm; ++j)
+      for (int i = lane; i < mm; i += 32) Fo.Rdel[i + j * MMAX] = (i < K - 1 && j < K - 1) ? Tw[i + j * MMAX] : 0.0;
   }
   if (lane == 0) Fo.has_del = 1;
   __syncwarp();
+  AA_TL(11);
 }
 
 template <int OP>
@@ -271,11 +288,11 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
       }
     }
   } else if constexpr (OP == OP_K2_ICWY) {
-    double* Tw = scratch;
-    double* v1 = scratch + MMAX * MMAX;
+    double* Tw = scratch + MMAX * MMAX;           // T' (staged)
+    double* v1 = Tw + MMAX * MMAX;
+    const double* r0s = scratch + SCR_R0;
     const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
-    icwy_assemble_T(p, red0, Tw, k);
-    for (int j = lane; j < k; j += 32) v1[j] = red0[L.off_df + j];
+    for (int j = lane; j < k; j += 32) v1[j] = r0s[L.off_df + j];
     __syncwarp();
     k3_forward_unit_lower(Tw, v1, k);   // Alg. 4 l.4
     for (int j = lane; j < k; j += 32) H.coef[j] = v1[j] * cur_scale(p, j);
@@ -483,9 +500,16 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   const int vb = p.vb;
 
   K4Head hd{};
+  if (blockIdx.x == 0) AA_TL(0);
+  if constexpr (OP == OP_K4 || OP == OP_K2_ICWY) {
+    stage_small<OP>(p, scratch);
+    __syncthreads();
+  }
+  if (blockIdx.x == 0) AA_TL(1);
   if constexpr (OP == OP_K4) {
     if (warp == 0) {
       hd = k4_head(p, H, scratch);
+      if (blockIdx.x == 0) AA_TL(8);
       if (blockIdx.x == 0) k4_write_next(p, H, scratch, hd);
     }
   } else {
@@ -496,6 +520,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     fence_mbar_init();
   }
   __syncthreads();
+  if (blockIdx.x == 0) AA_TL(2);
 
   const long long my_count =
       (ntiles > (long long)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -552,6 +577,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     const int rows = (int)min((long long)TR, n - row0);
     double* S = stage0 + sidx * stage_words;
     mbar_wait(&bars[sidx], par);
+    if (blockIdx.x == 0 && it == 0) AA_TL(3);
 
     // ------------------------------------------------------------ phase A (row-wise)
     for (int r = tid; r < TR; r += NT) {
@@ -745,6 +771,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   }
 
+  if (blockIdx.x == 0) AA_TL(4);
   // ------------------------------------------------------------ per-CTA partials
   double* mypart = p.part + (size_t)blockIdx.x * LRED;
   if constexpr (OP == OP_K1) {
@@ -812,24 +839,22 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   }
 
-  if constexpr (OP == OP_K4) {
-    // CTA 0: precompute QRDelete(R_new) for the next step (Givens + re-triangularised R)
-    if (blockIdx.x == 0) {
-      __syncthreads();
-      if (warp == 0) k4_precompute_delete(p, scratch);
-    }
-  }
-
+  if (blockIdx.x == 0) AA_TL(5);
   // ------------------------------------------------------------ cross-CTA reduction
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned int t = atomicAdd(&p.st->counter, 1u);
-    H.is_last = (t == gridDim.x - 1);
+  if (gridDim.x > 1) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned int t = atomicAdd(&p.st->counter, 1u);
+      H.is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!H.is_last) return;
+    __threadfence();
+  } else {
+    __syncthreads();   // one CTA: its own partials are visible after the barrier
   }
-  __syncthreads();
-  if (!H.is_last) return;
-  __threadfence();
+  AA_TL(6);   // last CTA
   double* outv = (OP == OP_K4) ? reinterpret_cast<double*>(H.scal) + 4 : p.red + (size_t)p.red_slot * LRED;
   for (int w = tid; w < p.words; w += NT) {
     double s = 0.0;
@@ -857,10 +882,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && gridDim.x > 1) {
     __threadfence();
     p.st->counter = 0u;
   }
+  AA_TL(7);
 }
 
 // counter-based SplitMix64 uniform generator (aa_testing.h), bitwise equal to

@@ -86,6 +86,7 @@ struct aa_ctx {
   void* xbuf = nullptr;                 // local [flags 4 KB][mailbox 2 x nranks x LRED]
   void* peer_base[MAX_RANKS] = {};
   unsigned long long seq = 0;
+  unsigned long long* tl = nullptr;   // test-only phase timeline (aa_test_timeline)
   bool inited = false;
   int failed = AA_OK;
   // options
@@ -365,6 +366,7 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   for (int i = 0; i < in.nvec; ++i) p.vec[i] = in.vec[i];
   const size_t smem = 0;
   p.st = c->st;
+  p.tl = c->tl;
   p.ver = c->ver;
   p.red = c->red;
   p.part = c->part;
@@ -523,6 +525,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   for (int i = 0; i < 5; ++i) c->logical_last[i] = 0;
 
   KParams p = base_params(c);
+  p.red_words0 = L.words;
   p.k = k;
   p.c_in = c_in;
   p.recycle = recycle ? 1 : 0;
@@ -939,6 +942,7 @@ int aa_delete_oldest(aa_handle_t h) {
   h->ar_last = 0;
   h->sp_last = 0;
   KParams p = base_params(h);
+  p.red_words0 = words;
   p.k = k;
   p.c_in = h->mi;
   p.recycle = 1;
@@ -1090,6 +1094,7 @@ int aa_destroy(aa_handle_t h) {
   for (int r = 0; r < MAX_RANKS; ++r)
     if (h->peer_base[r] && h->peer_base[r] != h->xbuf) cudaIpcCloseMemHandle(h->peer_base[r]);
   cudaFree(h->xbuf);
+  cudaFree(h->tl);
   if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
   cudaFree(h->Q);
   cudaFree(h->DG);
@@ -1166,6 +1171,24 @@ int aa_timings(aa_handle_t h, double* ms_out5, int64_t* counts5, int reset) {
 }
 
 int64_t aa_kernel_launches(aa_handle_t h) { return h ? h->launches : -1; }
+
+int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384) {
+  if (!h) return AA_ERR_ARG;
+  if (enable && !h->tl) {
+    CUDA_TRY(h, cudaMalloc(&h->tl, 384 * sizeof(unsigned long long)));
+    CUDA_TRY(h, cudaMemset(h->tl, 0, 384 * sizeof(unsigned long long)));
+  }
+  if (!enable && h->tl) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    cudaFree(h->tl);
+    h->tl = nullptr;
+  }
+  if (out384 && h->tl) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    CUDA_TRY(h, cudaMemcpy(out384, h->tl, 384 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
+  return AA_OK;
+}
 
 int aa_fill_uniform(double* out, int64_t n, int64_t offset, uint64_t seed, uint64_t stream, double lo,
                     double hi, void* cuda_stream) {

@@ -1,0 +1,46 @@
+// The K3 routines of aa_device.cuh in isolation (one working warp, shared memory), to
+// compare with their cost inside the K4 kernel (tools/timeline_probe.py).  Launch shapes:
+// 32 threads / small smem, 256 threads (warps 1..7 parked at a barrier), + 220 KB smem.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_2110_09667_b200/csrc/aa_device.cuh"
+using namespace aa;
+__global__ void k3(double* cs, double* sn, double* g, long long* cyc, int K) {
+  extern __shared__ double smem[];
+  double *R = smem, *W = R + MMAX * MMAX, *c = W + MMAX * MMAX, *gam = c + MMAX;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    for (int j = 0; j < MMAX; ++j)
+      for (int i = lane; i < MMAX; i += 32) R[i + j * MMAX] = (i <= j) ? 1.0 / (1 + i + j) + (i == j) : 0.0;
+    for (int i = lane; i < MMAX; i += 32) c[i] = 1.0 + i;
+    __syncwarp();
+    long long t0 = clock64();
+    k3_givens_delete(R, K, W, cs, sn);
+    long long t1 = clock64();
+    k3_back_subst(R, c, gam, K);
+    long long t2 = clock64();
+    k3_forward_unit_lower(R, c, K);
+    long long t3 = clock64();
+    if (lane < K) g[lane] = gam[lane] + c[lane];
+    if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; }
+  }
+  __syncthreads();
+}
+int main() {
+  double *cs, *sn, *g; long long* c;
+  cudaMalloc(&cs, 512); cudaMalloc(&sn, 512); cudaMalloc(&g, 512); cudaMalloc(&c, 64);
+  const int small = (2 * MMAX * MMAX + 2 * MMAX) * 8, big = 220 * 1024;
+  cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  struct { int thr, sm; const char* name; } shapes[] = {{32, small, "32thr/66KB"}, {256, small, "256thr/66KB"}, {256, big, "256thr/220KB"}};
+  for (auto s : shapes)
+    for (int K : {5, 20, 50}) {
+      long long h[3];
+      for (int r = 0; r < 2; ++r) {
+        k3<<<1, s.thr, s.sm>>>(cs, sn, g, c, K);
+        cudaMemcpy(h, c, 24, cudaMemcpyDeviceToHost);
+      }
+      printf("%-13s K=%d cycles: givens %lld (%.0f/step)  back_subst %lld  fwd %lld  [%s]\n", s.name, K, h[0],
+             h[0] / (double)(K - 1), h[1], h[2], cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
