@@ -25,6 +25,7 @@ paper's iteration counts at paper scale and DCGS-2-inside-AA trajectories,
 which the paper itself does not fix.
 """
 from .qr import (EPS, Ledger, QRState, Reducer, back_substitution,  # noqa: F401
-                 forward_substitution_unit_lower, icwy_rebuild_T, loss_of_orthogonality,
+                 forward_substitution_unit_lower, icwy_rebuild_T, icwy_update_T_small,
+                 loss_of_orthogonality,
                  qradd, qrdelete_givens, lsp_solve, VARIANTS)
 from .aa import aa_definition, aa_variant, AAResult  # noqa: F401

@@ -10,7 +10,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .qr import (Ledger, QRState, Reducer, back_substitution, icwy_rebuild_T,
+from .qr import (Ledger, QRState, Reducer, back_substitution, icwy_rebuild_T, icwy_update_T_small,
                  loss_of_orthogonality, lsp_solve, qradd, qrdelete_givens)
 
 
@@ -85,9 +85,12 @@ def aa_definition(G, x0: np.ndarray, m: int, max_iters: int, tol: float = 0.0,
 def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: float = 0.0,
                beta: float = 1.0, shards: int = 1, dcgs2_cond: int = 3,
                dcgs2_rscale: bool = False, record_x: bool = True, record_loo: bool = True,
-               dfs_override=None) -> AAResult:
+               dfs_override=None, icwy_delete: str = "rebuild") -> AAResult:
     """O2: Alg. 1 + Alg. 2 with the paper's incremental QR (variant in mgs/icwy/cgs2/dcgs2).
 
+    ``icwy_delete``: "rebuild" = the paper's T update after QRDelete, one reduction
+    (reading A6); "small" = the reduction-free variant icwy_update_T_small
+    (not in the paper).
     Ledger phases: qradd (Algs. 2 l.2, 3-6), qrdelete (ICWY rebuild),
     lsp_rhs (Alg. 2 l.9), norm_check (Alg. 1 l.8).
     Damping (reading A13): x_{i+1} = g_i - G_i gamma - (1-beta)(f_i - Q (Q^T f_i))."""
@@ -116,10 +119,13 @@ def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: flo
             st.mi = 1
         else:
             if i > m:                           # Alg. 2 l.4-5  QRDelete
-                qrdelete_givens(st)
+                rots = qrdelete_givens(st)
                 dG.popleft()
                 if variant == "icwy":
-                    icwy_rebuild_T(st, led, red)
+                    if icwy_delete == "small":
+                        icwy_update_T_small(st, rots)
+                    else:
+                        icwy_rebuild_T(st, led, red)
             qradd(variant, st, df, led, red, dcgs2_cond, dcgs2_rscale)   # Alg. 2 l.7
         dG.append(dg)
         k = st.mi

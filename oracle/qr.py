@@ -259,15 +259,17 @@ def qradd(variant: str, st: QRState, v: np.ndarray, led: Ledger, red: Reducer,
 # QRDelete (reading A7) and the ICWY T rebuild (A6)
 # --------------------------------------------------------------------------------------
 
-def qrdelete_givens(st: QRState) -> None:
+def qrdelete_givens(st: QRState) -> list:
     """Remove the oldest column of F = QR: drop R's first column (upper Hessenberg),
     re-triangularise with m_i - 1 Givens rotations of adjacent rows, apply the same
-    rotations to Q's columns, drop Q's last column.  No communication."""
+    rotations to Q's columns, drop Q's last column.  No communication.
+    Returns the rotations [(c_j, s_j)] in the order applied."""
     mi = st.mi
     if mi == 0:
         raise ValueError("qrdelete on an empty factorisation")
     H = np.array(st.R[:mi, 1:mi], copy=True)           # mi x (mi-1) upper Hessenberg
     Q = np.array(st.Q[:, :mi], copy=True)
+    rots = []
     for j in range(mi - 1):
         a, b = H[j, j], H[j + 1, j]
         rho = math.hypot(a, b)
@@ -280,6 +282,7 @@ def qrdelete_givens(st: QRState) -> None:
         H[j + 1, j:] = -s * hj + c * hj1
         H[j, j] = rho                                   # diagonal kept >= 0
         H[j + 1, j] = 0.0
+        rots.append((c, s))
         qj, qj1 = Q[:, j].copy(), Q[:, j + 1].copy()
         Q[:, j] = c * qj + s * qj1
         Q[:, j + 1] = -s * qj + c * qj1
@@ -288,6 +291,7 @@ def qrdelete_givens(st: QRState) -> None:
     st.Q[:, :mi - 1] = Q[:, :mi - 1]
     st.Q[:, mi - 1:] = 0.0
     st.mi = mi - 1
+    return rots
 
 
 def icwy_rebuild_T(st: QRState, led: Ledger, red: Reducer) -> None:
@@ -298,6 +302,33 @@ def icwy_rebuild_T(st: QRState, led: Ledger, red: Reducer) -> None:
     led.sync("qrdelete")
     st.T[:, :] = 0.0
     st.T[:k, :k] = np.eye(k) + np.tril(G, -1)
+
+
+def icwy_update_T_small(st: QRState, rots: list) -> None:
+    """VARIANT, not in the paper (reading A6b): after a
+    delete, update T without a reduction.  The delete replaced Q by Q' = Q W, W the first
+    m_i - 1 columns of the product of the rotations (applied to the identity exactly as
+    qrdelete_givens applies them to Q's columns), so Q'^T Q' = W^T (Q^T Q) W, and Q^T Q is
+    taken as S = T + T^T - I (unit diagonal) from the known rows of the pre-delete T.
+
+    Called after qrdelete_givens (st.mi = k retained columns).  Rows 0..k-2 of the new T
+    are set; row k-1 is left as the identity row because QRAdd (Alg. 4 l.1) recomputes it
+    before any use, and it would need the unknown T row of the newest pre-delete column."""
+    k = st.mi
+    mi = k + 1
+    W = np.eye(mi)
+    for j, (c, s) in enumerate(rots):
+        wj, wj1 = W[:, j].copy(), W[:, j + 1].copy()
+        W[:, j] = c * wj + s * wj1
+        W[:, j + 1] = -s * wj + c * wj1
+    Tk = st.T[:k, :k]                                    # known rows 0..k-1 (pre-delete)
+    S = Tk + Tk.T - np.eye(k)
+    Wp = W[:k, :k - 1]                                   # rows 0..k-1 suffice (column l uses rows <= l+1)
+    Sp = Wp.T @ S @ Wp
+    T = np.eye(k)
+    T[:k - 1, :k - 1] += np.tril(Sp, -1)
+    st.T[:, :] = 0.0
+    st.T[:k, :k] = T
 
 
 # --------------------------------------------------------------------------------------

@@ -16,7 +16,8 @@ import pytest
 import aa_inputs
 from aa_inputs import problems
 from oracle import (EPS, Ledger, QRState, Reducer, aa_definition, aa_variant, icwy_rebuild_T,
-                    loss_of_orthogonality, lsp_solve, qradd, qrdelete_givens, VARIANTS)
+                    icwy_update_T_small, loss_of_orthogonality, lsp_solve, qradd, qrdelete_givens,
+                    VARIANTS)
 from tests._gmres import gmres_iterates
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
@@ -259,6 +260,63 @@ def test_icwy_T_rebuild():
     st2.mi = 3
     icwy_rebuild_T(st2, Ledger(), Reducer(1))
     assert np.max(np.abs(st2.T - np.eye(3))) <= 1e-15
+
+
+def test_icwy_small_update_equals_gram_of_rotated_q():
+    """Reduction-free T update (variant): with unit-norm but
+    NON-orthogonal Q and T = I + strict_lower(Q^T Q) on the known rows 0..m_i-2, the
+    updated rows 0..k-2 equal the strict lower part of the explicit Gram of the rotated
+    Q' that qrdelete_givens produced (the paper's rebuild), and row k-1 is the
+    identity row.  Catches a wrong rotation sign or order, a transposed W, and an
+    off-by-one in the rows of T it reads."""
+    rng = np.random.default_rng(5)
+    n, mi = 40, 7
+    st = QRState(n, mi)
+    Q = rng.standard_normal((n, mi)) + 0.8 * rng.standard_normal((n, 1))   # correlated
+    Q /= np.linalg.norm(Q, axis=0)
+    st.Q[:, :] = Q
+    st.R[:, :] = np.triu(rng.standard_normal((mi, mi)))
+    st.R[np.diag_indices(mi)] = np.abs(np.diag(st.R)) + 1.0
+    G0 = Q.T @ Q
+    st.T[:, :] = np.eye(mi)
+    st.T[:mi - 1, :mi - 1] += np.tril(G0[:mi - 1, :mi - 1], -1)   # row mi-1 unknown
+    st.mi = mi
+    rots = qrdelete_givens(st)
+    assert len(rots) == mi - 1
+    icwy_update_T_small(st, rots)
+    k = st.mi
+    Qp = st.Q[:, :k]
+    Gp = Qp.T @ Qp
+    assert np.max(np.abs(G0 - np.eye(mi))) > 0.3          # the test is not vacuous
+    for i in range(k):
+        assert st.T[i, i] == 1.0
+        for j in range(k):
+            if i == k - 1 and j < i:
+                assert st.T[i, j] == 0.0
+            elif j < i:
+                assert abs(st.T[i, j] - Gp[i, j]) <= 1e-14, (i, j, st.T[i, j], Gp[i, j])
+            elif j > i:
+                assert st.T[i, j] == 0.0
+
+
+def test_icwy_small_update_aa_agrees_with_rebuild():
+    """AA with the reduction-free update follows the paper's rebuild to rounding on a
+    well-conditioned problem and needs no qrdelete reduction; on the SURVEY Pr6
+    ill-conditioned window (d in U[0.9, 0.99], LOO ~ 0.3) both converge."""
+    d, b = problems.diagonal(600, -0.9, 0.9)
+    G = lambda x: d * x + b
+    ra = aa_variant(G, np.zeros(600), 5, "icwy", 30)
+    rs = aa_variant(G, np.zeros(600), 5, "icwy", 30, icwy_delete="small")
+    for xa, xs in zip(ra.xs, rs.xs):
+        assert np.linalg.norm(xa - xs) <= 1e-10 * np.linalg.norm(xa)
+    assert ra.ledgers[-1]["qrdelete"] == 30 - 5 and rs.ledgers[-1]["qrdelete"] == 0
+    assert ra.ledgers[-1]["qradd"] == rs.ledgers[-1]["qradd"]
+    d2, b2 = problems.diagonal(4000, 0.9, 0.99, seed=11)
+    G2 = lambda x: d2 * x + b2
+    r2a = aa_variant(G2, np.zeros(4000), 20, "icwy", 80, record_x=False)
+    r2s = aa_variant(G2, np.zeros(4000), 20, "icwy", 80, record_x=False, icwy_delete="small")
+    f0 = r2a.f_norms[0]
+    assert r2a.f_norms[-1] <= 1e-9 * f0 and r2s.f_norms[-1] <= 1e-9 * f0, (r2a.f_norms[-1], r2s.f_norms[-1])
 
 
 # ----------------------------------------------------------------------------- AA driver
