@@ -32,6 +32,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "µs per AA iteration (QRAdd+LSP+update) and % HBM roofline at 1/2/4/8 B200"
 VARIANTS = ("dcgs2", "icwy", "cgs2", "mgs")
+# measured alongside the paper's four: ICWY with the reduction-free T update after QRDelete
+# (AA_OPT_ICWY_DELETE = SMALL; a variant, not in the paper: SURVEY.md §8(f) row 1)
+EXTRA_VARIANTS = ("icwy_small",)
+
+
+def split_variant(v):
+    """bench label -> (libaa variant, solver options)."""
+    if v == "icwy_small":
+        return "icwy", {"icwy_delete": 2}
+    return v, {}
 
 
 # --------------------------------------------------------------------- byte model (DESIGN.md)
@@ -48,7 +58,7 @@ def step_bytes(variant, m, V, beta_on=False):
     k4 = (m + 3) * V
     if variant == "dcgs2":
         k2 = (k + 4) * V if k >= 3 else (k + 3) * V
-    elif variant == "icwy":
+    elif variant in ("icwy", "icwy_small"):
         k2 = (k + 3) * V
     elif variant == "cgs2":
         k2 = (k + 2) * V + (k + 3) * V
@@ -304,7 +314,11 @@ def main():
         return s
 
     def measure(variant, m, steps, warmup, with_clocks=False, e2e=False):
-        s = make_solver(n_local, m, variant, profile=1, icwy_merged=args.icwy_merged)
+        base, extra = split_variant(variant)
+        extra.setdefault("icwy_merged", args.icwy_merged)
+        if "icwy_delete" in extra:
+            extra.pop("icwy_merged")
+        s = make_solver(n_local, m, base, profile=1, **extra)
         x = torch.zeros(n_local, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)
         s.init(x, G(x), xn)
@@ -378,7 +392,8 @@ def main():
         aa.aa_fill_uniform(dn, nl, -0.9, 0.9, stream_id=1, offset=rank * nl, stream=stream)
         aa.aa_fill_uniform(bn, nl, -1.0, 1.0, stream_id=2, offset=rank * nl, stream=stream)
         Gn = lambda x: torch.addcmul(bn, dn, x)
-        s = make_solver(nl, m, variant)
+        base, extra = split_variant(variant)
+        s = make_solver(nl, m, base, **extra)
         x = torch.zeros(nl, dtype=torch.float64, device="cuda")
         xn = torch.empty_like(x)
         s.init(x, Gn(x), xn)
@@ -408,7 +423,7 @@ def main():
                                 e2e=not args.no_e2e)
     variants = {}
     if not args.only_headline:
-        for v in VARIANTS:
+        for v in VARIANTS + EXTRA_VARIANTS:
             if v == args.variant:
                 r = head
             else:
@@ -422,7 +437,7 @@ def main():
     sweep = {}
     if args.sweep:
         for m in (5, 10, 20, 50):
-            for v in VARIANTS:
+            for v in VARIANTS + EXTRA_VARIANTS:
                 r, _, _ = measure(v, m, 3, 3)
                 sweep[f"{v}_m{m}"] = {"us_per_iter": r["ms_per_step"] * 1e3,
                                       "step_hbm_frac": step_bytes(v, m, V) / (r["ms_per_step"] * 1e-3) / (peak * 1e9),
@@ -431,7 +446,7 @@ def main():
     small_n = {}
     if args.sweep_n:
         for nl in (1000, 10000, 100000, 1500000, 10000000):
-            for v in VARIANTS:
+            for v in VARIANTS + EXTRA_VARIANTS:
                 small_n[f"{v}_n{nl}"] = measure_n(v, args.m, nl, 20, 5)
 
     k1b = k1_bytes(args.m, V)

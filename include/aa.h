@@ -75,7 +75,12 @@ enum aa_option {
                                   (not in the paper; reading A13)                */
     AA_OPT_ICWY_DELETE = 1,    /* 0 = SEPARATE (paper: T update after QRDelete is its own
                                   reduction; 3 allreduces per recycle iteration);
-                                  1 = MERGED into QRAdd's first reduction (2 allreduces)  */
+                                  1 = MERGED into QRAdd's first reduction (2 allreduces);
+                                  2 = SMALL: T' = I + strict_lower(W^T (T + T^T - I) W) from
+                                  the QRDelete rotations W, no Gram pass and no reduction
+                                  (2 allreduces; NOT in the paper: SURVEY.md §8(f) row 1,
+                                  DESIGN.md A6b).  Choosing SMALL after aa_init returns
+                                  AA_ERR_STATE; aa_delete_oldest always uses the rebuild. */
     AA_OPT_DCGS2_COND = 2,     /* reorthogonalise when m_i > val; paper: 3 (Alg. 6 l.2);
                                   2 is the shape-allowed alternative (reading A2)          */
     AA_OPT_DCGS2_RSCALE = 3,   /* 0 = R += s verbatim (Alg. 6 l.5); 1 = R += R_kk s (A3)  */

@@ -257,6 +257,11 @@ def aa_build_info() -> str:
     return buf.value.decode()
 
 
+# AA_OPT_ICWY_DELETE values (aa.h): the paper's rebuild as its own reduction, merged into
+# QRAdd's first reduction, or the reduction-free small-matrix update (variant, not in the paper)
+ICWY_DELETE_MODES = {"separate": 0, "merged": 1, "small": 2}
+
+
 # ------------------------------------------------------------------ convenience handle
 class AndersonSolver:
     """Owns one libaa handle.  Marshalling only (no arithmetic happens here)."""
@@ -268,11 +273,14 @@ class AndersonSolver:
             self.h = aa_create_with_comm(n_local, m, variant, rank, nranks, nccl_comm, stream)
         else:
             self.h = aa_create(n_local, m, variant, rank, nranks, unique_id, stream)
-        names = {"beta": OPT_DAMPING_BETA, "icwy_merged": OPT_ICWY_DELETE, "dcgs2_cond": OPT_DCGS2_COND,
+        names = {"beta": OPT_DAMPING_BETA, "icwy_merged": OPT_ICWY_DELETE, "icwy_delete": OPT_ICWY_DELETE,
+                 "dcgs2_cond": OPT_DCGS2_COND,
                  "dcgs2_rscale": OPT_DCGS2_RSCALE, "breakdown_eps": OPT_BREAKDOWN_EPS,
                  "profile": OPT_PROFILE, "n_global": OPT_N_GLOBAL, "fused_allreduce": OPT_FUSED_ALLREDUCE}
         for k, v in options.items():
             if v is not None:
+                if k == "icwy_delete" and isinstance(v, str):
+                    v = ICWY_DELETE_MODES[v]
                 aa_set_option(self.h, names[k], float(v))
 
     def init(self, x0, gx0, x1_out):

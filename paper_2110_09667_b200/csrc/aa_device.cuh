@@ -45,6 +45,7 @@ struct Factors {
   double R[MMAX * MMAX];     // column-major, leading dim MMAX, K x K valid
   double T[MMAX * MMAX];     // ICWY: I + L (reading A5), column-major
   double Rdel[MMAX * MMAX];  // R after QRDelete: (K-1) x (K-1)
+  double Tdel[MMAX * MMAX];  // ICWY_DELETE = SMALL: T after QRDelete, rows 0..K-3 (variant, A6b)
   double scale[MMAX];        // lazy normalisation: Q_j(true) = scale[j] * Q_j(stored)
   double gamma[MMAX];
   double cs[MMAX], sn[MMAX]; // Givens coefficients of QRDelete(R)
@@ -104,7 +105,7 @@ struct alignas(64) KParams {
   int gram;         // 0 none, 1 strict lower k x k (ICWY after delete), 2 lower incl. diag
   int reortho;      // DCGS-2 delayed reorthogonalisation active this step
   int rscale;       // DCGS-2 R update reading A3
-  int icwy_merged;  // (informational; layout is the same)
+  int icwy_merged;  // ICWY T update after QRDelete: 0 separate, 1 merged, 2 small-matrix (no Gram)
   int mgs_j;        // MGS pass index j (1..k)
   int final_slot;   // reduction slot holding (||v'||^2, v'^T f)
   int red_slot;     // slot this kernel writes
@@ -216,13 +217,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 // factor, re-triangularise the upper-Hessenberg remainder H = R[:, 1:] with mold-1 Givens
 // rotations of adjacent rows, rho = hypot(a,b) >= 0.  Output Rw ((mold-1)^2 upper
 // triangular, zeros below, col-major MMAX) and the rotation coefficients cs/sn (applied to
-// Q's columns by K1).
+// Q's columns by K1).  Rw may be global memory (K4 writes Fo.Rdel directly).
 // Register form: lane l owns Hessenberg columns l and l+32; "carry" is the column's entry
 // in the row being rotated (row j at step j), row j+1 is still the original R and is
 // prefetched one step ahead, so the serial chain per step is one shuffle, the hypot and
 // two products (no shared-memory round trip, no __syncwarp).
-__device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double* cs, double* sn,
-                                 unsigned long long* tsteps = nullptr) {
+__device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double* cs, double* sn) {
   const int lane = threadIdx.x & 31;
   const int nc = mold - 1;  // columns of the Hessenberg matrix
   const int l0 = lane, l1 = lane + 32;
@@ -232,7 +232,6 @@ __device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double*
   double h20 = h(1, l0), h21 = h(1, l1);
   double bn = (nc > 0) ? Rg[1 + 1 * MMAX] : 0.0;
   for (int j = 0; j < nc; ++j) {
-    if (tsteps && lane == 0) tsteps[j] = clock64();
     const double b = bn;                        // H[j+1][j], original
     const double n20 = h(j + 2, l0), n21 = h(j + 2, l1);   // next step's row j+2
     bn = (j + 1 < nc) ? Rg[(j + 2) + (j + 2) * MMAX] : 0.0;

@@ -103,6 +103,7 @@ __device__ void stage_small(const KParams& p, double* scratch) {
         else if (j > i) v = 0.0;
         else if (del_only) v = R0[i * (i - 1) / 2 + j];
         else if (i == k - 1) v = R0[L.off_x + j];
+        else if (p.recycle && p.icwy_merged == 2) v = F.Tdel[i + j * MMAX];
         else if (p.recycle) v = R0[L.off_gram + i * (i - 1) / 2 + j];
         else v = F.T[i + j * MMAX];
         Tw[i + j * MMAX] = v;
@@ -208,10 +209,12 @@ __device__ K4Head k4_scalars_head(const KParams& p) {
 
 // CTA 0 of K4 (warp 0): write factor version ver^1 from the head's results in shared
 // memory (Rw = R_new, Tw = T'; gamma in H.coef), then precompute QRDelete(R_new) for the
-// next step from the same shared copy (Givens work area: Tw, after T' is
-// written), so the next recycle step's heads only load it.
+// next step: the rotations (Fo.cs/sn) and R' (Fo.Rdel) go straight to
+// global memory, so the next recycle step's heads only load them.  ICWY_DELETE = SMALL
+// also precomputes the post-delete T (k4_tdel).
+__device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K);
+
 __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, const K4Head& hd) {
-  constexpr int OP = OP_K4;
   const int lane = threadIdx.x & 31;
   double* Rw = scratch;
   double* Tw = scratch + MMAX * MMAX;
@@ -243,17 +246,58 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
   }
   if (lane == 0) Fo.K = K;
   __syncwarp();
-  AA_TL(9);
-  // QRDelete of the new R, from shared memory
+  // QRDelete of the new R, from shared memory; R' straight to Fo.Rdel
   if (K >= 1) {
-    k3_givens_delete(Rw, K, Tw, Fo.cs, Fo.sn, p.tl ? p.tl + 256 : nullptr);
-    AA_TL(10);
-    for (int j = 0; j < mm; ++j)
-      for (int i = lane; i < mm; i += 32) Fo.Rdel[i + j * MMAX] = (i < K - 1 && j < K - 1) ? Tw[i + j * MMAX] : 0.0;
+    k3_givens_delete(Rw, K, Fo.Rdel, H.cs, H.sn);
+    for (int j = lane; j < K - 1; j += 32) {
+      Fo.cs[j] = H.cs[j];
+      Fo.sn[j] = H.sn[j];
+    }
+    if (p.variant == V_ICWY && p.icwy_merged == 2) k4_tdel(p, H, scratch, Fo, K);
   }
   if (lane == 0) Fo.has_del = 1;
   __syncwarp();
-  AA_TL(11);
+}
+
+// ICWY_DELETE = SMALL (variant, not in the paper, A6b):
+// the next QRDelete replaces Q by Q' = Q W (W = the rotations just computed, applied to
+// columns), so the post-delete Gram is W^T S W with S = T + T^T - I from the P = K-1 known
+// rows of T (Tw).  S is rotated two-sided in shared memory (Rw's area, leading dimension
+// MMAX+1 against bank conflicts): rotation j mixes columns then rows j, j+1; rotations
+// 0..P-2 fix every entry with both indices <= P-2, which are the rows the next step reads.
+__device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K) {
+  constexpr int LD = MMAX + 1;
+  const int lane = threadIdx.x & 31;
+  const double* Tw = scratch + MMAX * MMAX;
+  double* S = scratch;   // Rw is consumed (R_new written, QRDelete done): (MMAX-1) x LD fits
+  const int P = K - 1;
+  for (int j = 0; j < P; ++j)
+    for (int i = j + lane; i < P; i += 32) {
+      const double v = (i == j) ? 1.0 : Tw[i + j * MMAX];
+      S[i + j * LD] = v;
+      S[j + i * LD] = v;
+    }
+  __syncwarp();
+  for (int j = 0; j + 1 < P; ++j) {
+    const double c = H.cs[j], s = H.sn[j];
+    for (int i = lane; i < P; i += 32) {
+      const double a = S[i + j * LD], b = S[i + (j + 1) * LD];
+      S[i + j * LD] = c * a + s * b;
+      S[i + (j + 1) * LD] = -s * a + c * b;
+    }
+    __syncwarp();
+    for (int i = lane; i < P; i += 32) {
+      const double a = S[j + i * LD], b = S[(j + 1) + i * LD];
+      S[j + i * LD] = c * a + s * b;
+      S[(j + 1) + i * LD] = -s * a + c * b;
+    }
+    __syncwarp();
+  }
+  const int mm = p.m;
+  for (int j = 0; j < mm; ++j)
+    for (int i = lane; i < mm; i += 32)
+      Fo.Tdel[i + j * MMAX] = (i == j) ? 1.0 : ((j < i && i < P - 1) ? S[i + j * LD] : 0.0);
+  __syncwarp();
 }
 
 template <int OP>

@@ -518,7 +518,8 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   }
   const bool reortho = (V == V_DCGS2) && k >= 2 && (k + 1 > c->dcgs2_cond);
   const bool has_x = (V == V_ICWY && k >= 2) || (V == V_DCGS2 && reortho);
-  const int gram = (V == V_ICWY && recycle && k >= 2) ? 1 : 0;
+  // ICWY T update after QRDelete: the paper's Gram rebuild, unless SMALL (precomputed by K4)
+  const int gram = (V == V_ICWY && recycle && k >= 2 && c->icwy_merged != 2) ? 1 : 0;
   const K1Layout L = K1Layout::make(k, has_x, gram != 0);
   c->ar_last = 0;
   c->sp_last = 0;
@@ -651,7 +652,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   else if (V == V_CGS2) add = 3;
   else add = 2;
   c->logical_last[AA_PH_QRADD] = add;
-  c->logical_last[AA_PH_QRDELETE] = (V == V_ICWY && recycle) ? 1 : 0;
+  c->logical_last[AA_PH_QRDELETE] = (V == V_ICWY && recycle && c->icwy_merged != 2) ? 1 : 0;
   if (!ext) {
     c->logical_last[AA_PH_LSP_RHS] = 1;
     c->logical_last[AA_PH_NORM] = 1;
@@ -824,7 +825,9 @@ int aa_set_option(aa_handle_t h, int opt, double val) {
       h->beta = val;
       return AA_OK;
     case AA_OPT_ICWY_DELETE:
-      if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
+      if (val != 0.0 && val != 1.0 && val != 2.0) return AA_ERR_ARG;
+      // SMALL needs the post-delete T precomputed by the previous K4: choose it before aa_init
+      if (val == 2.0 && h->icwy_merged != 2 && h->inited) return AA_ERR_STATE;
       h->icwy_merged = (int)val;
       return AA_OK;
     case AA_OPT_DCGS2_COND:

@@ -20,7 +20,6 @@ for _ in range(3):
     s.step(x, g, xn); x, xn = xn, x
     tlc = aa.aa_test_timeline(s.h, True).astype(np.int64)
     tl, ck = tlc[0], tlc[1]
-    gsteps = aa.aa_test_timeline_raw(s.h)[256:256 + 64].astype(np.int64)
 names = ["entry", "staged", "head", "tile0", "tiles", "partials", "red", "end"]
 ops = {0: "K1", 1: "K2icwy", 2: "K2dcgs2", 3: "K2a", 4: "K2b", 5: "K2mgs", 6: "K4"}
 t0 = min(int(tl[o, 0]) for o in ops if tl[o, 0] > 0)
@@ -34,6 +33,4 @@ for o, nm in ops.items():
     # effective SM clock from clock64 deltas (CTA 0 slots 0..5 are on one SM)
     dt = tl[o, 5] - tl[o, 0]; dc = ck[o, 5] - ck[o, 0]
     if dt > 0: print(f"         SM clock over entry..partials: {dc / dt * 1e3:.0f} MHz ({dc} cycles)")
-    if o == 6:
-        print("         clock64 slots 8..11:", [int(ck[o, i] - ck[o, 9]) for i in range(8, 12)])
-        print("         givens step clocks (rel. slot 9):", [int(v - ck[o, 9]) for v in gsteps if v])
+
