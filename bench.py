@@ -359,9 +359,10 @@ def main():
         e2e_res = None
         if e2e:
             nh = 3
+            # all three host buffers pinned (empty_like does not inherit pinning)
             xh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
-            gh = torch.empty_like(xh)
-            outh = torch.empty_like(xh)
+            gh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+            outh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
             dh, bh = d.cpu(), b.cpu()
             xh.copy_(x.cpu())
             t_e = []

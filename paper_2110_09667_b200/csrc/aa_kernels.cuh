@@ -886,15 +886,18 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   if (blockIdx.x == 0) AA_TL(5);
   // ------------------------------------------------------------ cross-CTA reduction
   if (gridDim.x > 1) {
-    __threadfence();
+    // the barrier orders every thread's partial stores before thread 0's GPU-scope fence
+    // (fences are cumulative), which publishes them with the ticket; the last CTA's thread 0
+    // fences again (acquire side) before its CTA reads the partials through L2 (__ldcg)
     __syncthreads();
     if (tid == 0) {
+      __threadfence();
       const unsigned int t = atomicAdd(&p.st->counter, 1u);
       H.is_last = (t == gridDim.x - 1);
+      if (H.is_last) __threadfence();
     }
     __syncthreads();
     if (!H.is_last) return;
-    __threadfence();
   } else {
     __syncthreads();   // one CTA: its own partials are visible after the barrier
   }
@@ -925,11 +928,9 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       }
     }
   }
-  __syncthreads();
-  if (tid == 0 && gridDim.x > 1) {
-    __threadfence();
-    p.st->counter = 0u;
-  }
+  // every CTA has taken its ticket; the reset is ordered before the next launch by the
+  // kernel boundary
+  if (tid == 0 && gridDim.x > 1) p.st->counter = 0u;
   AA_TL(7);
 }
 
