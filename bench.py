@@ -434,7 +434,9 @@ def main():
                            "step_hbm_frac": bytes_step / (r["ms_per_step"] * 1e-3) / (peak * 1e9),
                            "k1_frac": k1_bytes(args.m, V) / (r["k1_ms"] * 1e-3) / (peak * 1e9),
                            "sync_points": r["sync_points_per_step"], "allreduces": r["allreduce_per_step"],
-                           "launches": r["launches_per_step"]}
+                           "launches": r["launches_per_step"], "k1_ms": r["k1_ms"],
+                           "k2_ms_per_step": r["k2_ms_per_step"], "k4_ms": r["k4_ms"],
+                           "allreduce_ms_per_step": r["allreduce_ms_per_step"], "ms_min": r["ms_min"]}
     sweep = {}
     if args.sweep:
         for m in (5, 10, 20, 50):

@@ -111,6 +111,8 @@ struct alignas(64) KParams {
   int red_slot;     // slot this kernel writes
   int words;        // words this kernel reduces
   int red_words0;   // words of reduction slot 0 the heads stage into shared memory
+  int pre_cta;      // K4 at small n: CTA 0 only writes the next factors + QRDelete precompute
+                    // (no tiles); tiles go to CTAs 1..gridDim-1
   unsigned long long* tl;   // test-only phase timeline (CTA 0 / last CTA, %globaltimer ns), or null
   int nin, tr, stages;
   int vb;           // first vector column (= sum of block columns)
@@ -213,47 +215,62 @@ __device__ __forceinline__ double warp_sum(double v) {
 // All routines run on ONE warp (lanes cooperate over columns / rows) with operands
 // in shared memory, leading dimension MMAX, and end with __syncwarp().
 
+// Leading dimension of R staged in shared memory: MMAX + 1, so that lane = column accesses
+// (R[i + l LDR] for l = lane) hit at most 2 banks instead of 32 (SHFL and LDS/STS share the
+// MIO pipe: conflicted accesses delay the shuffles on the serial chain).
+constexpr int LDR = MMAX + 1;
+
 // QRDelete on R (reading A7): drop column 0 of the mold x mold
 // factor, re-triangularise the upper-Hessenberg remainder H = R[:, 1:] with mold-1 Givens
-// rotations of adjacent rows, rho = hypot(a,b) >= 0.  Output Rw ((mold-1)^2 upper
-// triangular, zeros below, col-major MMAX) and the rotation coefficients cs/sn (applied to
-// Q's columns by K1).  Rw may be global memory (K4 writes Fo.Rdel directly).
+// rotations of adjacent rows, rho = hypot(a,b) >= 0.  Input leading dimension LDG; output
+// Rout ((mold-1)^2 upper triangular, zeros below, leading dimension MMAX; may be global
+// memory: K4 writes Fo.Rdel directly) and the rotation coefficients cs/sn (applied to Q's
+// columns by K1).
 // Register form: lane l owns Hessenberg columns l and l+32; "carry" is the column's entry
 // in the row being rotated (row j at step j), row j+1 is still the original R and is
-// prefetched one step ahead, so the serial chain per step is one shuffle, the hypot and
-// two products (no shared-memory round trip, no __syncwarp).
-__device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double* cs, double* sn) {
+// prefetched one step ahead, so the serial chain per step is one shuffle, one reciprocal
+// square root and a few products (no shared-memory round trip, no __syncwarp).
+// rho = t * t^{-1/2}, c = a t^{-1/2}, s = b t^{-1/2} with t = a^2 + b^2 after an exact
+// power-of-two scaling (one MUFU-seeded rsqrt instead of sqrt + reciprocal, no branches).
+template <int LDG>
+__device__ void k3_givens_delete(const double* Rg, int mold, double* Rout, double* cs, double* sn) {
   const int lane = threadIdx.x & 31;
   const int nc = mold - 1;  // columns of the Hessenberg matrix
   const int l0 = lane, l1 = lane + 32;
-  // H[i][l] = Rg[i + (l+1) MMAX] for i <= l+1 (R upper triangular), else 0
-  auto h = [&](int i, int l) -> double { return (l < nc && i <= l + 1) ? Rg[i + (l + 1) * MMAX] : 0.0; };
+  // H[i][l] = Rg[i + (l+1) LDG] for i <= l+1 (R upper triangular), else 0
+  auto h = [&](int i, int l) -> double { return (l < nc && i <= l + 1) ? Rg[i + (l + 1) * LDG] : 0.0; };
   double carry0 = h(0, l0), carry1 = h(0, l1);
   double h20 = h(1, l0), h21 = h(1, l1);
-  double bn = (nc > 0) ? Rg[1 + 1 * MMAX] : 0.0;
+  double bn = (nc > 0) ? Rg[1 + 1 * LDG] : 0.0;
   for (int j = 0; j < nc; ++j) {
     const double b = bn;                        // H[j+1][j], original
     const double n20 = h(j + 2, l0), n21 = h(j + 2, l1);   // next step's row j+2
-    bn = (j + 1 < nc) ? Rg[(j + 2) + (j + 2) * MMAX] : 0.0;
+    bn = (j + 1 < nc) ? Rg[(j + 2) + (j + 2) * LDG] : 0.0;
     const double a = __shfl_sync(0xffffffffu, j < 32 ? carry0 : carry1, j & 31);
-    // rho = hypot(a, b) >= 0; the plain form is exact to rounding unless a^2 + b^2 would
-    // over/underflow, where hypot's scaling takes over.  One reciprocal, two products.
-    const double aa = fabs(a), bb = fabs(b), mx = fmax(aa, bb);
-    const double rho = (mx < 1e150 && mx > 1e-150) ? sqrt(fma(a, a, b * b)) : hypot(a, b);
-    const double ri = rho > 0.0 ? 1.0 / rho : 0.0;
-    const double c = rho > 0.0 ? a * ri : 1.0;
-    const double s = rho > 0.0 ? b * ri : 0.0;
-    if (l0 > j && l0 < nc) {
-      Rw[j + l0 * MMAX] = __dadd_rn(__dmul_rn(c, carry0), __dmul_rn(s, h20));
-      carry0 = __dadd_rn(__dmul_rn(-s, carry0), __dmul_rn(c, h20));
-    }
-    if (l1 > j && l1 < nc) {
-      Rw[j + l1 * MMAX] = __dadd_rn(__dmul_rn(c, carry1), __dmul_rn(s, h21));
-      carry1 = __dadd_rn(__dmul_rn(-s, carry1), __dmul_rn(c, h21));
-    }
-    for (int i = j + 1 + lane; i < mold; i += 32) Rw[i + j * MMAX] = 0.0;   // column j below rho
+    // scale (a, b) by an exact power of two so that max(|a|,|b|) is in [1, 2): t = a'^2 + b'^2
+    // in [1, 8) needs no over/underflow branch; one rsqrt gives c, s and rho = t^{1/2} / 2^e
+    const double mx = fmax(fabs(a), fabs(b));
+    const int ex = (__double2hiint(mx) >> 20) & 0x7ff;             // biased exponent of mx
+    const int es = ex == 0 ? 1 : (ex == 0x7ff ? 0x7fe : ex);        // zero / denormal / inf guard
+    const double sc = __hiloint2double((2046 - es) << 20, 0);       // 2^(1023 - es), exact
+    const double usc = __hiloint2double(es << 20, 0);               // 2^(es - 1023), exact
+    const double as = a * sc, bs = b * sc;
+    const double t = fma(as, as, bs * bs);
+    const bool nz = mx > 0.0;
+    const double ri = rsqrt(nz ? t : 1.0);
+    const double rho = nz ? (t * ri) * usc : 0.0;
+    const double c = nz ? as * ri : 1.0;
+    const double s = nz ? bs * ri : 0.0;
+    const bool act0 = l0 > j && l0 < nc, act1 = l1 > j && l1 < nc;
+    const double o0 = __dadd_rn(__dmul_rn(c, carry0), __dmul_rn(s, h20));
+    const double o1 = __dadd_rn(__dmul_rn(c, carry1), __dmul_rn(s, h21));
+    carry0 = act0 ? __dadd_rn(__dmul_rn(-s, carry0), __dmul_rn(c, h20)) : carry0;
+    carry1 = act1 ? __dadd_rn(__dmul_rn(-s, carry1), __dmul_rn(c, h21)) : carry1;
+    if (act0) Rout[j + l0 * MMAX] = o0;
+    if (act1) Rout[j + l1 * MMAX] = o1;
+    for (int i = j + 1 + lane; i < mold; i += 32) Rout[i + j * MMAX] = 0.0;   // column j below rho
     if (lane == 0) {
-      Rw[j + j * MMAX] = rho;
+      Rout[j + j * MMAX] = rho;
       cs[j] = c;
       sn[j] = s;
     }
@@ -261,6 +278,30 @@ __device__ void k3_givens_delete(const double* Rg, int mold, double* Rw, double*
     h21 = n21;
   }
   __syncwarp();
+}
+
+// Two-sided application of the QRDelete rotations to a symmetric P x P matrix S in shared
+// memory (leading dimension LDS): S <- G_j^T S G_j for j = 0..P-2, where G_j mixes columns
+// (then rows) j and j+1 as K1 mixes Q's columns.  Entries with both indices <= P-2 are then
+// W^T S W restricted to them (the rotation P-1 would only touch row/column P-1).  One warp.
+template <int LDS>
+__device__ void k3_rotate_sym(double* S, int P, const double* cs, const double* sn) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j + 1 < P; ++j) {
+    const double c = cs[j], s = sn[j];
+    for (int i = lane; i < P; i += 32) {
+      const double a = S[i + j * LDS], b = S[i + (j + 1) * LDS];
+      S[i + j * LDS] = c * a + s * b;
+      S[i + (j + 1) * LDS] = -s * a + c * b;
+    }
+    __syncwarp();
+    for (int i = lane; i < P; i += 32) {
+      const double a = S[j + i * LDS], b = S[(j + 1) + i * LDS];
+      S[j + i * LDS] = c * a + s * b;
+      S[(j + 1) + i * LDS] = -s * a + c * b;
+    }
+    __syncwarp();
+  }
 }
 
 // Forward substitution with a unit lower-triangular T (Alg. 4 l.4 "T^{-1} R"; A5):
@@ -285,21 +326,23 @@ __device__ void k3_forward_unit_lower(const double* T, double* r, int k) {
   __syncwarp();
 }
 
-// Back substitution R gamma = c (Alg. 2 l.9), R upper triangular K x K; c overwritten.
+// Back substitution R gamma = c (Alg. 2 l.9), R upper triangular K x K (leading dimension
+// LD); c overwritten.
 // Lane i holds c_i (and c_{i+32}) and 1/R_ii; step j: lane j forms gamma_j, one shuffle
 // broadcasts it, every lane updates its c_i with R's column j (prefetched a step ahead).
+template <int LD>
 __device__ void k3_back_subst(const double* R, double* c, double* gamma, int K) {
   const int lane = threadIdx.x & 31;
   const int i0 = lane, i1 = lane + 32;
   double c0 = (i0 < K) ? c[i0] : 0.0, c1 = (i1 < K) ? c[i1] : 0.0;
   // reciprocals of the diagonal in parallel, so the serial chain has no division
-  const double rinv0 = (i0 < K) ? 1.0 / R[i0 + i0 * MMAX] : 0.0;
-  const double rinv1 = (i1 < K) ? 1.0 / R[i1 + i1 * MMAX] : 0.0;
-  double r0 = (i0 < K && K > 0) ? R[i0 + (K - 1) * MMAX] : 0.0;
-  double r1 = (i1 < K && K > 0) ? R[i1 + (K - 1) * MMAX] : 0.0;
+  const double rinv0 = (i0 < K) ? 1.0 / R[i0 + i0 * LD] : 0.0;
+  const double rinv1 = (i1 < K) ? 1.0 / R[i1 + i1 * LD] : 0.0;
+  double r0 = (i0 < K && K > 0) ? R[i0 + (K - 1) * LD] : 0.0;
+  double r1 = (i1 < K && K > 0) ? R[i1 + (K - 1) * LD] : 0.0;
   for (int j = K - 1; j >= 0; --j) {
-    const double rn0 = (i0 < j && j >= 1) ? R[i0 + (j - 1) * MMAX] : 0.0;
-    const double rn1 = (i1 < j && j >= 1) ? R[i1 + (j - 1) * MMAX] : 0.0;
+    const double rn0 = (i0 < j && j >= 1) ? R[i0 + (j - 1) * LD] : 0.0;
+    const double rn1 = (i1 < j && j >= 1) ? R[i1 + (j - 1) * LD] : 0.0;
     const double mine = (j < 32) ? c0 * rinv0 : c1 * rinv1;
     const double gj = __shfl_sync(0xffffffffu, mine, j & 31);
     if (lane == 0) gamma[j] = gj;

@@ -58,8 +58,11 @@ __host__ __device__ constexpr size_t head_bytes() { return align_up(sizeof(HeadA
 __host__ __device__ constexpr size_t bar_bytes() { return 128; }
 // scratch for the head / commit (aliases the stage ring before and after the pipeline)
 // scratch (aliases the stage ring before / after the pipeline):
-// [Rw MMAX^2][Tw MMAX^2][v1, cvec, cvec2, spare: 4 x MMAX][R0: copy of reduction slot 0][RF: 8 words]
-constexpr size_t SCR_R0 = 2 * MMAX * MMAX + 4 * MMAX;
+// [Rw MMAX x LDR][Tw MMAX^2][v1, cvec, cvec2, spare: 4 x MMAX][R0: copy of reduction slot 0]
+// [RF: 8 words]
+constexpr size_t SCR_TW = (size_t)MMAX * LDR;
+constexpr size_t SCR_V = SCR_TW + MMAX * MMAX;
+constexpr size_t SCR_R0 = SCR_V + 4 * MMAX;
 constexpr size_t SCR_RF = SCR_R0 + LRED;
 __host__ __device__ constexpr size_t scratch_bytes() { return (SCR_RF + 8) * sizeof(double); }
 
@@ -80,7 +83,7 @@ __device__ void stage_small(const KParams& p, double* scratch) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
   double* Rw = scratch;
-  double* Tw = scratch + MMAX * MMAX;
+  double* Tw = scratch + SCR_TW;
   double* R0 = scratch + SCR_R0;
   double* RF = scratch + SCR_RF;
   const int nw = (OP == OP_K4 || OP == OP_K2_ICWY) ? p.red_words0 : 0;
@@ -90,7 +93,7 @@ __device__ void stage_small(const KParams& p, double* scratch) {
   if constexpr (OP == OP_K4) {
     const double* Rsrc = p.recycle ? F.Rdel : F.R;
     for (int j = warp; j < k; j += NWARP)
-      for (int i = lane; i < k; i += 32) Rw[i + j * MMAX] = Rsrc[i + j * MMAX];
+      for (int i = lane; i < k; i += 32) Rw[i + j * LDR] = Rsrc[i + j * MMAX];
   }
   if (p.variant == V_ICWY && (OP == OP_K4 || OP == OP_K2_ICWY)) {
     __syncthreads();   // R0 complete
@@ -121,9 +124,9 @@ struct K4Head {
 // back-substitution.  Writes Rw (K x K), Tw (ICWY), gamma into H.coef, c into cvec.
 __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   const int lane = threadIdx.x & 31;
-  double* Rw = scratch;                 // R' (staged by stage_small)
-  double* Tw = scratch + MMAX * MMAX;   // ICWY T' (staged)
-  double* v1 = Tw + MMAX * MMAX;        // MMAX words
+  double* Rw = scratch;                 // R' (staged by stage_small), leading dimension LDR
+  double* Tw = scratch + SCR_TW;        // ICWY T' (staged)
+  double* v1 = scratch + SCR_V;         // MMAX words
   double* cvec = v1 + MMAX;             // MMAX
   double* cvec2 = cvec + MMAX;          // MMAX
   const double* red0 = scratch + SCR_R0;
@@ -143,26 +146,26 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
     for (int j = lane; j < k; j += 32) v1[j] = red0[L.off_df + j];
     __syncwarp();
     k3_forward_unit_lower(Tw, v1, k);
-    for (int j = lane; j < k; j += 32) Rw[j + k * MMAX] = v1[j];
+    for (int j = lane; j < k; j += 32) Rw[j + k * LDR] = v1[j];
   } else {
     for (int j = lane; j < k; j += 32) {
       double r;
       if (p.variant == V_MGS) r = (j == 0) ? red0[L.off_df] : p.red[j * LRED];
       else if (p.variant == V_CGS2) r = red0[L.off_df + j] + p.red[LRED + j];   // s + z (Alg. 5 l.5)
       else r = red0[L.off_df + j];                                               // DCGS-2 l.1 (A4)
-      Rw[j + k * MMAX] = r;
+      Rw[j + k * LDR] = r;
     }
   }
   __syncwarp();
   if (p.variant == V_DCGS2 && p.reortho) {  // Alg. 6 l.5 (verbatim R += s, or A3)
-    const double rk1 = Rw[(k - 1) + (k - 1) * MMAX];
+    const double rk1 = Rw[(k - 1) + (k - 1) * LDR];
     for (int j = lane; j < k - 1; j += 32) {
       const double s = red0[L.off_x + j];
-      Rw[j + (k - 1) * MMAX] += p.rscale ? rk1 * s : s;
+      Rw[j + (k - 1) * LDR] += p.rscale ? rk1 * s : s;
     }
   }
-  if (lane == 0) Rw[k + k * MMAX] = rkk;
-  for (int i = lane; i < k; i += 32) Rw[k + i * MMAX] = 0.0;
+  if (lane == 0) Rw[k + k * LDR] = rkk;
+  for (int i = lane; i < k; i += 32) Rw[k + i * LDR] = 0.0;
   // c = Q^T f_i with the final Q
   for (int j = lane; j < k; j += 32) cvec[j] = red0[L.off_f + j];
   __syncwarp();
@@ -176,7 +179,7 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   __syncwarp();
   for (int j = lane; j <= k; j += 32) cvec2[j] = cvec[j];
   __syncwarp();
-  k3_back_subst(Rw, cvec2, H.coef, k + 1);  // gamma -> H.coef[0..k]
+  k3_back_subst<LDR>(Rw, cvec2, H.coef, k + 1);  // gamma -> H.coef[0..k]
   if (p.beta_on) {
     for (int j = lane; j <= k; j += 32) {
       double fs;
@@ -217,7 +220,7 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
 __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, const K4Head& hd) {
   const int lane = threadIdx.x & 31;
   double* Rw = scratch;
-  double* Tw = scratch + MMAX * MMAX;
+  double* Tw = scratch + SCR_TW;
   const Factors& Fi = p.st->f[p.ver];
   Factors& Fo = p.st->f[p.ver ^ 1];
   const int K = hd.K;
@@ -225,7 +228,7 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
   const bool del_only = p.flags & F_DELETE_ONLY;
   for (int j = 0; j < mm; ++j)
     for (int i = lane; i < mm; i += 32) {
-      Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * MMAX] : 0.0;
+      Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * LDR] : 0.0;
       if (p.variant == V_ICWY) {
         double v = 0.0;
         if (i == j) v = (i < K) ? 1.0 : 0.0;
@@ -248,7 +251,7 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
   __syncwarp();
   // QRDelete of the new R, from shared memory; R' straight to Fo.Rdel
   if (K >= 1) {
-    k3_givens_delete(Rw, K, Fo.Rdel, H.cs, H.sn);
+    k3_givens_delete<LDR>(Rw, K, Fo.Rdel, H.cs, H.sn);
     for (int j = lane; j < K - 1; j += 32) {
       Fo.cs[j] = H.cs[j];
       Fo.sn[j] = H.sn[j];
@@ -268,8 +271,8 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
 __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K) {
   constexpr int LD = MMAX + 1;
   const int lane = threadIdx.x & 31;
-  const double* Tw = scratch + MMAX * MMAX;
-  double* S = scratch;   // Rw is consumed (R_new written, QRDelete done): (MMAX-1) x LD fits
+  const double* Tw = scratch + SCR_TW;
+  double* S = scratch;   // Rw's area (R_new written, QRDelete done): MMAX x LD
   const int P = K - 1;
   for (int j = 0; j < P; ++j)
     for (int i = j + lane; i < P; i += 32) {
@@ -278,21 +281,7 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
       S[j + i * LD] = v;
     }
   __syncwarp();
-  for (int j = 0; j + 1 < P; ++j) {
-    const double c = H.cs[j], s = H.sn[j];
-    for (int i = lane; i < P; i += 32) {
-      const double a = S[i + j * LD], b = S[i + (j + 1) * LD];
-      S[i + j * LD] = c * a + s * b;
-      S[i + (j + 1) * LD] = -s * a + c * b;
-    }
-    __syncwarp();
-    for (int i = lane; i < P; i += 32) {
-      const double a = S[j + i * LD], b = S[(j + 1) + i * LD];
-      S[j + i * LD] = c * a + s * b;
-      S[(j + 1) + i * LD] = -s * a + c * b;
-    }
-    __syncwarp();
-  }
+  k3_rotate_sym<LD>(S, P, H.cs, H.sn);
   const int mm = p.m;
   for (int j = 0; j < mm; ++j)
     for (int i = lane; i < mm; i += 32)
@@ -332,8 +321,8 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
       }
     }
   } else if constexpr (OP == OP_K2_ICWY) {
-    double* Tw = scratch + MMAX * MMAX;           // T' (staged)
-    double* v1 = Tw + MMAX * MMAX;
+    double* Tw = scratch + SCR_TW;                // T' (staged)
+    double* v1 = scratch + SCR_V;
     const double* r0s = scratch + SCR_R0;
     const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
     for (int j = lane; j < k; j += 32) v1[j] = r0s[L.off_df + j];
@@ -566,12 +555,14 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   __syncthreads();
   if (blockIdx.x == 0) AA_TL(2);
 
-  const long long my_count =
-      (ntiles > (long long)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // tile CTAs: all, or (K4 pre_cta) all but CTA 0, which only did the factor precompute
+  const int pre = (OP == OP_K4) ? p.pre_cta : 0;
+  const long long tb = (long long)blockIdx.x - pre, tg = (long long)gridDim.x - pre;
+  const long long my_count = (tb >= 0 && ntiles > tb) ? (ntiles - 1 - tb) / tg + 1 : 0;
   if (lane == 0) {
     fence_proxy_async();
     for (int s = 0; s < NS && s < my_count; ++s) {
-      const long long t = blockIdx.x + (long long)s * gridDim.x;
+      const long long t = tb + (long long)s * tg;
       const long long r0 = t * TR;
       issue_tile_part(p, stage0 + s * stage_words, &bars[s], r0, (int)min((long long)TR, n - r0), warp);
     }
@@ -616,7 +607,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   for (long long it = 0; it < my_count; ++it) {
     const int sidx = (int)(it % NS);
     const uint32_t par = (uint32_t)((it / NS) & 1);
-    const long long tile = blockIdx.x + it * gridDim.x;
+    const long long tile = tb + it * tg;
     const long long row0 = tile * TR;
     const int rows = (int)min((long long)TR, n - row0);
     double* S = stage0 + sidx * stage_words;
@@ -809,7 +800,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     __syncthreads();
     if (lane == 0 && it + NS < my_count) {
       fence_proxy_async();
-      const long long t2 = blockIdx.x + (it + NS) * gridDim.x;
+      const long long t2 = tb + (it + NS) * tg;
       const long long r2 = t2 * TR;
       issue_tile_part(p, S, &bars[sidx], r2, (int)min((long long)TR, n - r2), warp);
     }

@@ -321,6 +321,14 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const long long ntiles = (p.n + p.tr - 1) / p.tr;
   long long grid = std::min<long long>(ntiles, (long long)c->sms * per_sm);
   if (grid < 1) grid = 1;
+  // K4 when the tiles do not fill the GPU: one extra CTA (CTA 0) writes the next factor
+  // version and precomputes the next QRDelete while the others run gamma + the x update,
+  // so that serial work leaves the kernel's critical path
+  p.pre_cta = 0;
+  if (OP == OP_K4 && ntiles >= 1 && ntiles + 1 <= (long long)c->sms * per_sm) {
+    p.pre_cta = 1;
+    grid = ntiles + 1;
+  }
   {
     EvScope ev(c, cls);
     aa_stream_kernel<OP, NCW, G><<<(unsigned)grid, NT, smem, c->stream>>>(p);

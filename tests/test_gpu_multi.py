@@ -33,7 +33,10 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
     n, m, iters = 100003, 5, 14
     d, b = problems.diagonal(n)
     for variant, r in rep["variants"].items():
-        o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters)
+        if variant == "icwy_small":   # reduction-free post-delete T update (A6b)
+            o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, "icwy", iters, icwy_delete="small")
+        else:
+            o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters)
         for a, ref in zip(r["xs"], o2.xs):
             assert np.linalg.norm(np.array(a) - ref) <= 1e-10 * np.linalg.norm(ref), variant
         for a, ref in zip(r["f_norms"], o2.f_norms):
@@ -44,9 +47,9 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
         assert ars[0] == 1
         for i in range(2, iters + 1):
             if i <= m:
-                want = {"mgs": i, "icwy": 2, "cgs2": 3, "dcgs2": 2}[variant]
+                want = {"mgs": i, "icwy": 2, "cgs2": 3, "dcgs2": 2, "icwy_small": 2}[variant]
             else:
-                want = {"mgs": m, "icwy": 3, "cgs2": 3, "dcgs2": 2}[variant]
+                want = {"mgs": m, "icwy": 3, "cgs2": 3, "dcgs2": 2, "icwy_small": 2}[variant]
             assert ars[i - 1] == want, (variant, i, ars)
         assert r["gamma_identical_across_ranks"]
         assert r["loo"] < 1e-12

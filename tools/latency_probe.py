@@ -8,8 +8,10 @@ stream = torch.cuda.current_stream()
 d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
 b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
 G = lambda x: torch.addcmul(b, d, x)
-for v in ("dcgs2", "icwy", "cgs2", "mgs"):
-    s = aa.AndersonSolver(n, m, v, stream=stream, profile=1)
+VS = sys.argv[3].split(",") if len(sys.argv) > 3 else ["dcgs2", "icwy", "cgs2", "mgs"]
+for v in VS:
+    s = aa.AndersonSolver(n, m, "icwy" if v == "icwy_small" else v, stream=stream, profile=1,
+                          icwy_delete="small" if v == "icwy_small" else None)
     x = torch.zeros(n, dtype=torch.float64, device="cuda"); xn = torch.empty_like(x)
     s.init(x, G(x), xn); x, xn = xn, x
     for _ in range(m + 5):

@@ -1,8 +1,8 @@
 #!/bin/bash
 # ncu launch list (pure kernel durations) of the small-n latency probe; prints medians.
-N=${1:-1000}; M=${2:-20}
-python tools/latency_probe.py $N $M > /dev/null 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sn_launches.csv python tools/latency_probe.py $N $M > /dev/null 2>&1
+N=${1:-1000}; M=${2:-20}; V=${3:-dcgs2,icwy,cgs2,mgs}
+python tools/latency_probe.py $N $M $V > /dev/null 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sn_launches.csv python tools/latency_probe.py $N $M $V > /dev/null 2>&1
 python - <<'PY'
 import csv, re
 from collections import defaultdict

@@ -19,8 +19,9 @@ for n in ns:
     e1.record(); torch.cuda.synchronize()
     tg = e0.elapsed_time(e1) / K * 1e3
     out = [f"n={n:>8d} m={m} G {tg:5.1f} us |"]
-    for v in ("dcgs2", "icwy", "cgs2", "mgs"):
-        s = aa.AndersonSolver(n, m, v, stream=stream)
+    for v in ("dcgs2", "icwy", "icwy_small", "cgs2", "mgs"):
+        s = aa.AndersonSolver(n, m, "icwy" if v == "icwy_small" else v, stream=stream,
+                              icwy_delete="small" if v == "icwy_small" else None)
         x.zero_()
         s.init(x, torch.addcmul(b, d, x), xn); x, xn = xn, x
         for _ in range(m + 10):
