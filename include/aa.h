@@ -87,12 +87,26 @@ enum aa_option {
     AA_OPT_BREAKDOWN_EPS = 4,  /* eps_a; default 10 * DBL_EPSILON * sqrt(n_global)        */
     AA_OPT_PROFILE = 5,        /* 1 = record per-kernel CUDA events (aa_timings)           */
     AA_OPT_N_GLOBAL = 6,       /* global vector length (for the default eps_a)             */
-    AA_OPT_FUSED_ALLREDUCE = 7 /* 1 = every global reduction is a one-shot exchange done by
+    AA_OPT_FUSED_ALLREDUCE = 7, /* 1 = every global reduction is a one-shot exchange done by
                                   the producing kernel's last CTA over NVLink peer memory
                                   (CUDA IPC, same node) instead of ncclAllReduce; collective
                                   (all ranks set it); 0 = ncclAllReduce (default).  If the
                                   IPC setup fails the call returns its error and the handle
                                   keeps using ncclAllReduce (not sticky)                    */
+    AA_OPT_CONV_NORM = 8,      /* ||x_{i+1} - x_i|| of Alg. 1 l.8:
+                                  0 = LAGGED (default): the local partial rides in the next
+                                  step's first reduction; aa_stats sums it over ranks on
+                                  demand (one extra allreduce per aa_stats call if p > 1).
+                                  1 = IMMEDIATE: aa_step performs that allreduce itself
+                                  (one more physical reduction per iteration, as the paper's
+                                  loop checks the norm every iteration).
+                                  2 = OFF: not reported (aa_stats dx_norm = -1), no
+                                  norm_check in the ledger.                                 */
+    AA_OPT_DETERMINISTIC = 9   /* reductions are always summed in a fixed order (per-CTA
+                                  partials in CTA order, ranks in rank order), so results
+                                  are bitwise reproducible for a given n_local, m, variant
+                                  and rank count; 1 (default) and 0 are both accepted and
+                                  change nothing.                                            */
 };
 
 /* aa_stats flags */

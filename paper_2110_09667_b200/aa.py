@@ -18,6 +18,7 @@ MGS, ICWY, CGS2, DCGS2 = 0, 1, 2, 3
 VARIANT_IDS = {"mgs": MGS, "icwy": ICWY, "cgs2": CGS2, "dcgs2": DCGS2}
 OPT_DAMPING_BETA, OPT_ICWY_DELETE, OPT_DCGS2_COND, OPT_DCGS2_RSCALE = 0, 1, 2, 3
 OPT_BREAKDOWN_EPS, OPT_PROFILE, OPT_N_GLOBAL, OPT_FUSED_ALLREDUCE = 4, 5, 6, 7
+OPT_CONV_NORM, OPT_DETERMINISTIC = 8, 9
 STATS_LOO, STATS_RESET = 1, 2
 AA_OK, AA_ERR_BREAKDOWN = 0, 6
 PHASES = ("qradd", "qrdelete", "lsp_rhs", "norm_check", "other")
@@ -260,6 +261,8 @@ def aa_build_info() -> str:
 # AA_OPT_ICWY_DELETE values (aa.h): the paper's rebuild as its own reduction, merged into
 # QRAdd's first reduction, or the reduction-free small-matrix update (variant, not in the paper)
 ICWY_DELETE_MODES = {"separate": 0, "merged": 1, "small": 2}
+# AA_OPT_CONV_NORM values (aa.h)
+CONV_NORM_MODES = {"lagged": 0, "immediate": 1, "off": 2}
 
 
 # ------------------------------------------------------------------ convenience handle
@@ -276,11 +279,14 @@ class AndersonSolver:
         names = {"beta": OPT_DAMPING_BETA, "icwy_merged": OPT_ICWY_DELETE, "icwy_delete": OPT_ICWY_DELETE,
                  "dcgs2_cond": OPT_DCGS2_COND,
                  "dcgs2_rscale": OPT_DCGS2_RSCALE, "breakdown_eps": OPT_BREAKDOWN_EPS,
-                 "profile": OPT_PROFILE, "n_global": OPT_N_GLOBAL, "fused_allreduce": OPT_FUSED_ALLREDUCE}
+                 "profile": OPT_PROFILE, "n_global": OPT_N_GLOBAL, "fused_allreduce": OPT_FUSED_ALLREDUCE,
+                 "conv_norm": OPT_CONV_NORM, "deterministic": OPT_DETERMINISTIC}
         for k, v in options.items():
             if v is not None:
                 if k == "icwy_delete" and isinstance(v, str):
                     v = ICWY_DELETE_MODES[v]
+                if k == "conv_norm" and isinstance(v, str):
+                    v = CONV_NORM_MODES[v]
                 aa_set_option(self.h, names[k], float(v))
 
     def init(self, x0, gx0, x1_out):

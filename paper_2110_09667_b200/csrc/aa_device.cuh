@@ -55,7 +55,9 @@ struct Factors {
 
 struct SmallState {
   Factors f[2];
+  // ---- scalar tail (aa_stats copies only this part)
   double dx2_local;          // this rank's ||x_{i+1} - x_i||^2 from the last update
+  double dx2_global;         // CONV_NORM = IMMEDIATE: the same, summed over ranks by aa_step
   double f2;                 // ||f_i||^2 (global) of the last step
   double rratio_min;         // min R_kk / ||Delta f||
   double last_rkk;
@@ -222,30 +224,33 @@ constexpr int LDR = MMAX + 1;
 
 // QRDelete on R (reading A7): drop column 0 of the mold x mold
 // factor, re-triangularise the upper-Hessenberg remainder H = R[:, 1:] with mold-1 Givens
-// rotations of adjacent rows, rho = hypot(a,b) >= 0.  Input leading dimension LDG; output
-// Rout ((mold-1)^2 upper triangular, zeros below, leading dimension MMAX; may be global
-// memory: K4 writes Fo.Rdel directly) and the rotation coefficients cs/sn (applied to Q's
-// columns by K1).
+// rotations of adjacent rows, rho = hypot(a,b) >= 0.  IN PLACE in shared memory (leading
+// dimension LD): on return R's columns 0..mold-2 hold R' in their upper triangle (entries
+// below the diagonal are left stale; callers copy the triangle), and cs/sn (shared) the
+// rotation coefficients (applied to Q's columns by K1).
 // Register form: lane l owns Hessenberg columns l and l+32; "carry" is the column's entry
 // in the row being rotated (row j at step j), row j+1 is still the original R and is
 // prefetched one step ahead, so the serial chain per step is one shuffle, one reciprocal
-// square root and a few products (no shared-memory round trip, no __syncwarp).
+// square root and a few products.  Step j writes row j of columns j+1.. and rho into
+// (j, j): no lane reads those again, and with LD = MMAX + 1 the column-per-lane stores
+// hit at most two banks (they share the MIO pipe with the shuffle).
 // rho = t * t^{-1/2}, c = a t^{-1/2}, s = b t^{-1/2} with t = a^2 + b^2 after an exact
 // power-of-two scaling (one MUFU-seeded rsqrt instead of sqrt + reciprocal, no branches).
-template <int LDG>
-__device__ void k3_givens_delete(const double* Rg, int mold, double* Rout, double* cs, double* sn) {
+template <int LD>
+__device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn) {
   const int lane = threadIdx.x & 31;
   const int nc = mold - 1;  // columns of the Hessenberg matrix
   const int l0 = lane, l1 = lane + 32;
-  // H[i][l] = Rg[i + (l+1) LDG] for i <= l+1 (R upper triangular), else 0
-  auto h = [&](int i, int l) -> double { return (l < nc && i <= l + 1) ? Rg[i + (l + 1) * LDG] : 0.0; };
+  // H[i][l] = R[i + (l+1) LD] for i <= l+1 (R upper triangular), else 0
+  auto h = [&](int i, int l) -> double { return (l < nc && i <= l + 1) ? R[i + (l + 1) * LD] : 0.0; };
   double carry0 = h(0, l0), carry1 = h(0, l1);
   double h20 = h(1, l0), h21 = h(1, l1);
-  double bn = (nc > 0) ? Rg[1 + 1 * LDG] : 0.0;
+  double bn = (nc > 0) ? R[1 + 1 * LD] : 0.0;
+  __syncwarp();
   for (int j = 0; j < nc; ++j) {
     const double b = bn;                        // H[j+1][j], original
     const double n20 = h(j + 2, l0), n21 = h(j + 2, l1);   // next step's row j+2
-    bn = (j + 1 < nc) ? Rg[(j + 2) + (j + 2) * LDG] : 0.0;
+    bn = (j + 1 < nc) ? R[(j + 2) + (j + 2) * LD] : 0.0;
     const double a = __shfl_sync(0xffffffffu, j < 32 ? carry0 : carry1, j & 31);
     // scale (a, b) by an exact power of two so that max(|a|,|b|) is in [1, 2): t = a'^2 + b'^2
     // in [1, 8) needs no over/underflow branch; one rsqrt gives c, s and rho = t^{1/2} / 2^e
@@ -266,11 +271,10 @@ __device__ void k3_givens_delete(const double* Rg, int mold, double* Rout, doubl
     const double o1 = __dadd_rn(__dmul_rn(c, carry1), __dmul_rn(s, h21));
     carry0 = act0 ? __dadd_rn(__dmul_rn(-s, carry0), __dmul_rn(c, h20)) : carry0;
     carry1 = act1 ? __dadd_rn(__dmul_rn(-s, carry1), __dmul_rn(c, h21)) : carry1;
-    if (act0) Rout[j + l0 * MMAX] = o0;
-    if (act1) Rout[j + l1 * MMAX] = o1;
-    for (int i = j + 1 + lane; i < mold; i += 32) Rout[i + j * MMAX] = 0.0;   // column j below rho
+    if (act0) R[j + l0 * LD] = o0;              // R'[j][l] (R' column l = R column l)
+    if (act1) R[j + l1 * LD] = o1;
     if (lane == 0) {
-      Rout[j + j * MMAX] = rho;
+      R[j + j * LD] = rho;
       cs[j] = c;
       sn[j] = s;
     }
@@ -281,24 +285,43 @@ __device__ void k3_givens_delete(const double* Rg, int mold, double* Rout, doubl
 }
 
 // Two-sided application of the QRDelete rotations to a symmetric P x P matrix S in shared
-// memory (leading dimension LDS): S <- G_j^T S G_j for j = 0..P-2, where G_j mixes columns
-// (then rows) j and j+1 as K1 mixes Q's columns.  Entries with both indices <= P-2 are then
-// W^T S W restricted to them (the rotation P-1 would only touch row/column P-1).  One warp.
+// memory (leading dimension LDS, both triangles stored): S <- G_j^T S G_j for j = 0..P-2,
+// where G_j mixes columns (then rows) j and j+1 as K1 mixes Q's columns.  Entries with both
+// indices <= P-2 are then W^T S W restricted to them (rotation P-1 would only touch row /
+// column P-1).  One pass per rotation: lane i (i != j, j+1) rotates (S[i][j], S[i][j+1]) and
+// writes both symmetric copies; one lane updates the 2 x 2 diagonal block in closed form.
 template <int LDS>
 __device__ void k3_rotate_sym(double* S, int P, const double* cs, const double* sn) {
   const int lane = threadIdx.x & 31;
+  const int i0 = lane, i1 = lane + 32;
   for (int j = 0; j + 1 < P; ++j) {
     const double c = cs[j], s = sn[j];
-    for (int i = lane; i < P; i += 32) {
-      const double a = S[i + j * LDS], b = S[i + (j + 1) * LDS];
-      S[i + j * LDS] = c * a + s * b;
-      S[i + (j + 1) * LDS] = -s * a + c * b;
-    }
+    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+    const bool u0 = i0 < P && i0 != j && i0 != j + 1, u1 = i1 < P && i1 != j && i1 != j + 1;
+    if (u0) { a0 = S[i0 + j * LDS]; b0 = S[i0 + (j + 1) * LDS]; }
+    if (u1) { a1 = S[i1 + j * LDS]; b1 = S[i1 + (j + 1) * LDS]; }
+    double p = 0.0, q = 0.0, r = 0.0;
+    if (lane == 0) { p = S[j + j * LDS]; q = S[(j + 1) + j * LDS]; r = S[(j + 1) + (j + 1) * LDS]; }
     __syncwarp();
-    for (int i = lane; i < P; i += 32) {
-      const double a = S[j + i * LDS], b = S[(j + 1) + i * LDS];
-      S[j + i * LDS] = c * a + s * b;
-      S[(j + 1) + i * LDS] = -s * a + c * b;
+    if (u0) {
+      const double na = c * a0 + s * b0, nb = -s * a0 + c * b0;
+      S[i0 + j * LDS] = na;  S[i0 + (j + 1) * LDS] = nb;
+      S[j + i0 * LDS] = na;  S[(j + 1) + i0 * LDS] = nb;
+    }
+    if (u1) {
+      const double na = c * a1 + s * b1, nb = -s * a1 + c * b1;
+      S[i1 + j * LDS] = na;  S[i1 + (j + 1) * LDS] = nb;
+      S[j + i1 * LDS] = na;  S[(j + 1) + i1 * LDS] = nb;
+    }
+    if (lane == 0) {   // [p q; q r] -> G^T [p q; q r] G
+      const double cc = c * c, ss = s * s, cs2 = 2.0 * c * s;
+      const double pn = cc * p + cs2 * q + ss * r;
+      const double rn = ss * p - cs2 * q + cc * r;
+      const double qn = (cc - ss) * q + c * s * (r - p);
+      S[j + j * LDS] = pn;
+      S[(j + 1) + (j + 1) * LDS] = rn;
+      S[(j + 1) + j * LDS] = qn;
+      S[j + (j + 1) * LDS] = qn;
     }
     __syncwarp();
   }

@@ -212,9 +212,9 @@ __device__ K4Head k4_scalars_head(const KParams& p) {
 
 // CTA 0 of K4 (warp 0): write factor version ver^1 from the head's results in shared
 // memory (Rw = R_new, Tw = T'; gamma in H.coef), then precompute QRDelete(R_new) for the
-// next step: the rotations (Fo.cs/sn) and R' (Fo.Rdel) go straight to
-// global memory, so the next recycle step's heads only load them.  ICWY_DELETE = SMALL
-// also precomputes the post-delete T (k4_tdel).
+// next step: the rotations (Fo.cs/sn) and R' (Fo.Rdel), so the next
+// recycle step's heads only load them.  ICWY_DELETE = SMALL also precomputes the
+// post-delete T (k4_tdel).
 __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K);
 
 __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, const K4Head& hd) {
@@ -249,13 +249,17 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
   }
   if (lane == 0) Fo.K = K;
   __syncwarp();
-  // QRDelete of the new R, from shared memory; R' straight to Fo.Rdel
+  // QRDelete of the new R, in place in shared memory, then R' and the rotations to Fo
   if (K >= 1) {
-    k3_givens_delete<LDR>(Rw, K, Fo.Rdel, H.cs, H.sn);
+    k3_givens_delete<LDR>(Rw, K, H.cs, H.sn);
+    for (int j = 0; j < mm; ++j)
+      for (int i = lane; i < mm; i += 32)
+        Fo.Rdel[i + j * MMAX] = (i <= j && j < K - 1) ? Rw[i + j * LDR] : 0.0;
     for (int j = lane; j < K - 1; j += 32) {
       Fo.cs[j] = H.cs[j];
       Fo.sn[j] = H.sn[j];
     }
+    __syncwarp();
     if (p.variant == V_ICWY && p.icwy_merged == 2) k4_tdel(p, H, scratch, Fo, K);
   }
   if (lane == 0) Fo.has_del = 1;
@@ -525,6 +529,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   double* scratch = stage0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // programmatic dependent launch: this grid may be resident before its predecessor on the
+  // stream has finished; wait for it (and its memory) before touching anything it wrote,
+  // then let the next kernel start launching (it waits the same way)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long n = p.n;
   const int TR = p.tr, NS = p.stages;
   const size_t stage_words = align_up((size_t)p.nin * TR, 16);

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -92,6 +93,7 @@ struct aa_ctx {
   // options
   double beta = 1.0, eps_a = -1.0;
   int icwy_merged = 0, dcgs2_cond = 3, dcgs2_rscale = 0, profile = 0;
+  int conv_norm = 0;   // AA_OPT_CONV_NORM: 0 lagged, 1 immediate, 2 off
   // ledger
   int64_t logical[5] = {0, 0, 0, 0, 0}, logical_last[5] = {0, 0, 0, 0, 0};
   int64_t ar_total = 0;
@@ -331,7 +333,20 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   }
   {
     EvScope ev(c, cls);
-    aa_stream_kernel<OP, NCW, G><<<(unsigned)grid, NT, smem, c->stream>>>(p);
+    // programmatic dependent launch (griddepcontrol in the kernel): the launch and CTA
+    // ramp-up overlap the predecessor's tail; AA_NO_PDL=1 disables it (A/B measurements)
+    static const bool pdl = !(getenv("AA_NO_PDL") && atoi(getenv("AA_NO_PDL")) != 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, aa_stream_kernel<OP, NCW, G>, p));
   }
   c->launches++;
   CUDA_TRY(c, cudaGetLastError());
@@ -651,6 +666,13 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     }
     RET_IF(launch_op<OP_K4>(c, q, in, 2));
   }
+  // CONV_NORM = IMMEDIATE: ||x_{i+1} - x_i||^2 summed over ranks now (Alg. 1 l.8 every step)
+  if (!ext && c->conv_norm == 1 && c->nranks > 1) {
+    double* d2 = &c->st->dx2_global;
+    CUDA_TRY(c, cudaMemcpyAsync(d2, &c->st->dx2_local, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    RET_IF(allreduce(c, d2, 1));
+    c->sp_last++;
+  }
   c->ver ^= 1;
   c->mi = k + 1;
   // ---------------- ledger (paper's logical counts)
@@ -663,7 +685,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   c->logical_last[AA_PH_QRDELETE] = (V == V_ICWY && recycle && c->icwy_merged != 2) ? 1 : 0;
   if (!ext) {
     c->logical_last[AA_PH_LSP_RHS] = 1;
-    c->logical_last[AA_PH_NORM] = 1;
+    c->logical_last[AA_PH_NORM] = (c->conv_norm == 2) ? 0 : 1;
   }
   for (int i = 0; i < 5; ++i) c->logical[i] += c->logical_last[i];
   return AA_OK;
@@ -865,6 +887,13 @@ int aa_set_option(aa_handle_t h, int opt, double val) {
       }
       h->fused = (int)val;
       return AA_OK;
+    case AA_OPT_CONV_NORM:
+      if (val != 0.0 && val != 1.0 && val != 2.0) return AA_ERR_ARG;
+      h->conv_norm = (int)val;
+      return AA_OK;
+    case AA_OPT_DETERMINISTIC:
+      if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
+      return AA_OK;   // always deterministic (fixed-order sums)
     default:
       return AA_ERR_ARG;
   }
@@ -1013,21 +1042,28 @@ int aa_stats(aa_handle_t h, struct aa_stats* out, int flags) {
     int bd;
   } hs;
   {
-    SmallState* full = new SmallState();
-    cudaError_t e = cudaMemcpy(full, h->st, sizeof(SmallState), cudaMemcpyDeviceToHost);
-    hs.dx2 = full->dx2_local;
-    hs.f2 = full->f2;
-    hs.rmin = full->rratio_min;
-    hs.bd = full->breakdown;
-    const int xto = full->xchg_timeout;
-    delete full;
+    // only the scalar tail of SmallState (the factors stay on the device)
+    constexpr size_t off = offsetof(SmallState, dx2_local);
+    unsigned char tail[sizeof(SmallState) - off];
+    cudaError_t e = cudaMemcpy(tail, reinterpret_cast<unsigned char*>(h->st) + off, sizeof(tail),
+                               cudaMemcpyDeviceToHost);
+    CUDA_TRY(h, e);
+    auto fld = [&](size_t o) { return tail + (o - off); };
+    double dx2l, dx2g;
+    int xto;
+    memcpy(&dx2l, fld(offsetof(SmallState, dx2_local)), sizeof(double));
+    memcpy(&dx2g, fld(offsetof(SmallState, dx2_global)), sizeof(double));
+    memcpy(&hs.f2, fld(offsetof(SmallState, f2)), sizeof(double));
+    memcpy(&hs.rmin, fld(offsetof(SmallState, rratio_min)), sizeof(double));
+    memcpy(&hs.bd, fld(offsetof(SmallState, breakdown)), sizeof(int));
+    memcpy(&xto, fld(offsetof(SmallState, xchg_timeout)), sizeof(int));
+    hs.dx2 = (h->conv_norm == 1 && h->nranks > 1) ? dx2g : dx2l;
     if (xto) {
       fprintf(stderr, "libaa: fused peer exchange timed out\n");
       return fail(h, AA_ERR_NCCL);
     }
-    CUDA_TRY(h, e);
   }
-  if (h->nranks > 1) {
+  if (h->nranks > 1 && h->conv_norm == 0) {
     double* tmp = h->red + (size_t)(NSLOT - 1) * LRED;
     CUDA_TRY(h, cudaMemcpyAsync(tmp, &hs.dx2, sizeof(double), cudaMemcpyHostToDevice, h->stream));
     ncclResult_t r = nccl().AllReduce(tmp, tmp, 1, kNcclFloat64, kNcclSum, h->comm, h->stream);
@@ -1036,7 +1072,7 @@ int aa_stats(aa_handle_t h, struct aa_stats* out, int flags) {
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   }
   out->f_norm = sqrt(hs.f2);
-  out->dx_norm = sqrt(hs.dx2);
+  out->dx_norm = (h->conv_norm == 2) ? -1.0 : sqrt(hs.dx2);
   out->r_ratio_min = hs.rmin;
   out->breakdown = hs.bd;
   if ((flags & AA_STATS_LOO) && h->mi >= 1) {

@@ -35,6 +35,8 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
     for variant, r in rep["variants"].items():
         if variant == "icwy_small":   # reduction-free post-delete T update (A6b)
             o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, "icwy", iters, icwy_delete="small")
+        elif variant == "dcgs2_immediate":   # AA_OPT_CONV_NORM = IMMEDIATE
+            o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, "dcgs2", iters)
         else:
             o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters)
         for a, ref in zip(r["xs"], o2.xs):
@@ -44,12 +46,15 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
         # one ncclAllReduce per global reduction: FIRST 1; start-up MGS m_i, ICWY 2,
         # CGS-2 3, DCGS-2 2; recycle MGS m, ICWY 3, CGS-2 3, DCGS-2 2
         ars = r["allreduce_per_step"]
+        if variant == "dcgs2_immediate":   # the convergence norm is one more allreduce per step
+            ars = [a - 1 for a in ars]
+            assert r["dx_norms"] == rep["variants"]["dcgs2"]["dx_norms"]
         assert ars[0] == 1
         for i in range(2, iters + 1):
             if i <= m:
-                want = {"mgs": i, "icwy": 2, "cgs2": 3, "dcgs2": 2, "icwy_small": 2}[variant]
+                want = {"mgs": i, "icwy": 2, "cgs2": 3, "dcgs2": 2, "icwy_small": 2, "dcgs2_immediate": 2}[variant]
             else:
-                want = {"mgs": m, "icwy": 3, "cgs2": 3, "dcgs2": 2, "icwy_small": 2}[variant]
+                want = {"mgs": m, "icwy": 3, "cgs2": 3, "dcgs2": 2, "icwy_small": 2, "dcgs2_immediate": 2}[variant]
             assert ars[i - 1] == want, (variant, i, ars)
         assert r["gamma_identical_across_ranks"]
         assert r["loo"] < 1e-12

@@ -345,3 +345,22 @@ def test_no_writes_outside_caller_buffers(n):
         if not s.stats().breakdown:      # n = 1: every later Delta f is dependent (R_kk = 0)
             assert torch.isfinite(xn).all()
         s.close()
+
+
+def test_conv_norm_options():
+    """AA_OPT_CONV_NORM: OFF reports no ||x_{i+1}-x_i|| and no norm_check in the ledger;
+    IMMEDIATE and LAGGED give the same norms (1 rank: no extra reduction)."""
+    n, m, iters = 5000, 4, 10
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    lag = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, "dcgs2", iters)
+    imm = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, "dcgs2", iters, conv_norm="immediate")
+    off = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, "dcgs2", iters, conv_norm="off")
+    assert imm.dx_norms == lag.dx_norms and imm.sync_points == lag.sync_points
+    assert all(v == -1.0 for v in off.dx_norms)
+    assert off.ledgers[-1]["norm_check"] == 0 and lag.ledgers[-1]["norm_check"] == iters
+    for a, c in zip(off.xs, lag.xs):
+        assert np.array_equal(a, c)
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, "dcgs2", iters)
+    for a, r in zip(lag.dx_norms, o2.dx_norms):
+        assert abs(a - r) <= 1e-10 * r + 1e-15

@@ -16,7 +16,9 @@ __global__ void k3(double* cs, double* sn, double* g, long long* cyc, int K, con
     for (int i = lane; i < MMAX; i += 32) c[i] = 1.0 + i;
     __syncwarp();
     long long t0 = clock64();
-    k3_givens_delete<LDR>(R, K, W, cs, sn);   // output ld MMAX (as K4's Fo.Rdel)
+    double* scs0 = gam + MMAX;
+    double* ssn0 = scs0 + MMAX;
+    k3_givens_delete<LDR>(R, K, scs0, ssn0);   // in place (as K4)
     long long t1 = clock64();
     k3_back_subst<LDR>(R, c, gam, K);
     long long t2 = clock64();
@@ -26,9 +28,9 @@ __global__ void k3(double* cs, double* sn, double* g, long long* cyc, int K, con
     for (int j = 0; j < K; ++j)
       for (int i = lane; i < K; i += 32) W[i + j * LDR] = (i == j) ? 1.0 : 0.01 * (1 + ((i + j) % 7));
     __syncwarp();
-    double* scs = gam + MMAX;
-    double* ssn = scs + MMAX;
-    for (int i = lane; i < K; i += 32) { scs[i] = cs[i]; ssn[i] = sn[i]; }
+    double* scs = scs0;
+    double* ssn = ssn0;
+    for (int i = lane; i < K; i += 32) { cs[i] = scs[i]; sn[i] = ssn[i]; }
     __syncwarp();
     long long t4 = clock64();
     k3_rotate_sym<LDR>(W, K - 1, scs, ssn);
