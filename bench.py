@@ -355,7 +355,7 @@ def main():
                "allreduce_ms_per_step": max_over_ranks(ms_t[3] / steps),
                "launches_per_step": launches / steps, "launches": launches,
                "sync_points_per_step": st.sync_points_last, "allreduce_per_step": st.allreduce_last,
-               "f_norm": st.f_norm}
+               "f_norm": st.f_norm, "step_ms": [round(v, 4) for v in step_ms]}
         e2e_res = None
         if e2e:
             nh = 3
@@ -436,7 +436,8 @@ def main():
                            "sync_points": r["sync_points_per_step"], "allreduces": r["allreduce_per_step"],
                            "launches": r["launches_per_step"], "k1_ms": r["k1_ms"],
                            "k2_ms_per_step": r["k2_ms_per_step"], "k4_ms": r["k4_ms"],
-                           "allreduce_ms_per_step": r["allreduce_ms_per_step"], "ms_min": r["ms_min"]}
+                           "allreduce_ms_per_step": r["allreduce_ms_per_step"], "ms_min": r["ms_min"],
+                           "step_ms_rank0": r["step_ms"]}
     sweep = {}
     if args.sweep:
         for m in (5, 10, 20, 50):

@@ -726,7 +726,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           const double v = v0 + v1;
           p.Q[(size_t)k * p.ld + grow] = v;  // y (Alg. 5 l.2), in place
           S[(size_t)k * TR + r] = v;
-          for (int jj = 0; jj < k; ++jj) S[(size_t)jj * TR + r] *= H.sc[jj];
+          // phase B dots the STORED columns with y; the lazy scales are applied to the
+          // per-CTA partials (z_j = sc_j * sum_r Q_stored[r][j] y[r])
         }
         // rows past n: the tensor copy zero-filled every column
       } else if constexpr (OP == OP_K2_MGS) {
@@ -856,7 +857,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       const int a = warp + c * NWARP;
       if (NCW > 0 && a < H.na) {
         const double v = warp_sum(acc[c][0]);
-        if (lane == 0) mypart[a] = v;
+        if (lane == 0) mypart[a] = v * H.sc[a];   // lazy scale of column a (lcol[a] = a)
       }
     }
   } else if constexpr (OP == OP_GRAM) {

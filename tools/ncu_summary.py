@@ -120,7 +120,10 @@ def full(src, name, tag):
     rows = list(csv.reader(raw.splitlines()))
     if len(rows) < 3:
         return f"(no data in {rep})"
-    d = dict(zip(rows[0], rows[2]))
+    return "\n\n".join(_full_one(dict(zip(rows[0], r)), name, tag) for r in rows[2:])
+
+
+def _full_one(d, name, tag):
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
@@ -128,8 +131,8 @@ def full(src, name, tag):
             "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__shared_mem_per_block_dynamic"]
-    lines = [f"# {tag}: `ncu --set full` of {name} (n_local = 2e7, m = 20, recycle)", "",
-             "| metric | value |", "|---|---|"]
+    lines = [f"# {tag}: `ncu --set full` of {name} (n_local = 2e7, m = 20, recycle): "
+             f"{d.get('Kernel Name', '')[:60]}", "", "| metric | value |", "|---|---|"]
     for kk in keys:
         if kk in d:
             lines.append(f"| {kk} | {d[kk]} |")
@@ -155,8 +158,9 @@ def main():
             "| kernel | DRAM GB/launch | algorithmic GB | ratio | ncu ms | ncu GB/s |", "|---|---|---|---|---|---|"]
     r1, t_d = traffic(src, "traffic.csv", 20, "dcgs2")
     r2, t_i = traffic(src, "traffic_icwy.csv", 20, "icwy")
-    open(os.path.join(dst, "traffic.md"), "w").write("\n".join(rows + r1 + r2) + "\n")
-    for name in ("k1_dcgs2", "k1_icwy"):
+    r3 = traffic(src, "traffic_cgs2.csv", 20, "cgs2")[0] if os.path.exists(os.path.join(src, "traffic_cgs2.csv")) else []
+    open(os.path.join(dst, "traffic.md"), "w").write("\n".join(rows + r1 + r2 + r3) + "\n")
+    for name in ("k1_dcgs2", "k1_icwy", "k2_cgs2"):
         if os.path.exists(os.path.join(src, name + ".ncu-rep")):
             open(os.path.join(dst, name + ".md"), "w").write(full(src, name, tag) + "\n")
     summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")

@@ -21,6 +21,9 @@ echo "traffic $?"
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
     --csv --log-file $OUT/traffic_icwy.csv $H --variant icwy > $OUT/traffic_icwy.log 2>&1
 echo "traffic_icwy $?"
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    --csv --log-file $OUT/traffic_cgs2.csv $H --variant cgs2 > $OUT/traffic_cgs2.log 2>&1
+echo "traffic_cgs2 $?"
 S="python bench.py --only-headline --no-e2e --no-cpu --n-local 2e7 --steps 3 --warmup 3"
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:stream_kernel<.int.0," -s 22 -c 1 -o $OUT/k1_dcgs2 $S > $OUT/k1_dcgs2.log 2>&1
@@ -28,3 +31,6 @@ echo "k1_dcgs2 $?"
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:stream_kernel<.int.0," -s 22 -c 1 -o $OUT/k1_icwy $S --variant icwy > $OUT/k1_icwy.log 2>&1
 echo "k1_icwy $?"
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k "regex:stream_kernel<.int.[34]," -s 44 -c 2 -o $OUT/k2_cgs2 $S --variant cgs2 > $OUT/k2_cgs2.log 2>&1
+echo "k2_cgs2 $?"
