@@ -137,9 +137,7 @@ struct alignas(64) KParams {
   int xoff[2], xcnt[2];
   unsigned long long seq0;
   double* pmbox[MAX_RANKS];               // peer q's mailbox (q == rank: local)
-  unsigned long long* pflags[MAX_RANKS];  // peer q's flag array
   double* lmbox;
-  unsigned long long* lflags;
   double* red;      // reduction slots (slot s at red + s*LRED)
   double* part;     // per-CTA partials (CTA b at part + b*LRED)
 };

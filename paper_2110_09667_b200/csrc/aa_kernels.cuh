@@ -468,51 +468,64 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// relaxed system-scope 8-byte accesses: an aligned 8-byte store is single-copy atomic, so
+// a word that carries its own sequence tag needs no fence and no separate flag
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* ptr, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* ptr) {
   unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ptr) : "memory");
   return v;
 }
 
 // One-shot allreduce of v[0..cnt) among the node's ranks, run by the LAST CTA of a kernel
-// on every rank ("fused local + global reduction"):
-// push v into slot [seq&1][rank] of every peer's mailbox through NVLink, publish seq in
-// the peer's flag[rank] (release, system scope), wait until every flag[q] >= seq
-// (acquire), then sum the p vectors in rank order -- the same order on every rank, so all
-// ranks obtain bitwise identical sums.  Double-buffered by seq parity: a peer reaches
-// seq+2 only after this rank has published seq+1, i.e. after it finished reading seq.
+// on every rank ("fused local + global reduction"), over
+// NVLink peer memory with a low-latency protocol: every fp64 word travels as two 8-byte
+// stores, each carrying 32 data bits and the exchange's 32-bit sequence tag, into every
+// rank's mailbox [seq parity][source rank][word][half]; a reader spins on the words
+// themselves until both halves carry the tag -- no fence, no flag round trip.  The p
+// vectors are summed in rank order, the same order on every rank, so all ranks obtain
+// bitwise identical sums.  A slot of parity s&1 is rewritten only by exchange s+2, which
+// no rank can start before every rank has read exchange s (it needs all of s+1 first).
 // The wait is time-bounded (10 s): on timeout a sticky flag is set instead of hanging.
 __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned long long seq) {
   const int tid = threadIdx.x;
+  const int R = p.nranks;
   const int par = (int)(seq & 1ull);
-  const size_t slot = (size_t)(par * p.nranks + p.rank) * LRED;
-  for (int q = 0; q < p.nranks; ++q) {
-    double* dst = p.pmbox[q] + slot;
-    for (int w = tid; w < cnt; w += NT) dst[w] = v[w];
+  const unsigned long long tag = (seq & 0xffffffffull) << 32;
+  for (int i = tid; i < cnt * R; i += NT) {
+    const int q = i / cnt, w = i - q * cnt;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v[w]);
+    unsigned long long* dst =
+        reinterpret_cast<unsigned long long*>(p.pmbox[q]) + ((size_t)(par * R + p.rank) * LRED + w) * 2;
+    st_relaxed_sys_u64(dst, tag | (bits & 0xffffffffull));
+    st_relaxed_sys_u64(dst + 1, tag | (bits >> 32));
   }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence_system();
-    for (int q = 0; q < p.nranks; ++q) st_release_sys(p.pflags[q] + p.rank, seq);
-  }
-  if (tid < p.nranks) {
-    const unsigned long long t0 = global_ns();
-    while (ld_acquire_sys(p.lflags + tid) < seq) {
-      if (global_ns() - t0 > 10000000000ull) {
-        p.st->xchg_timeout = 1;
-        break;
-      }
-    }
-  }
-  __syncthreads();
+  __syncthreads();   // every v[w] has been read before it is overwritten below
+  const unsigned long long* lm = reinterpret_cast<const unsigned long long*>(p.lmbox);
+  bool timed_out = false;
   for (int w = tid; w < cnt; w += NT) {
     double s = 0.0;
-    for (int q = 0; q < p.nranks; ++q) s += __ldcg(p.lmbox + (size_t)(par * p.nranks + q) * LRED + w);
+    for (int q = 0; q < R; ++q) {
+      const unsigned long long* src = lm + ((size_t)(par * R + q) * LRED + w) * 2;
+      unsigned long long lo, hi;
+      unsigned int spins = 0;
+      const unsigned long long t0 = global_ns();
+      while (true) {
+        lo = ld_relaxed_sys_u64(src);
+        hi = ld_relaxed_sys_u64(src + 1);
+        if ((lo & 0xffffffff00000000ull) == tag && (hi & 0xffffffff00000000ull) == tag) break;
+        if ((++spins & 1023u) == 0 && global_ns() - t0 > 10000000000ull) {
+          timed_out = true;
+          break;
+        }
+      }
+      s += __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+    }
     v[w] = s;
   }
+  if (timed_out) p.st->xchg_timeout = 1;
   __syncthreads();
 }
 

@@ -487,11 +487,7 @@ void plan_ar(aa_ctx* c, KParams& q, int o0, int n0, int o1, int n1) {
       ++q.nxchg;
     }
   c->seq += q.nxchg;
-  for (int r = 0; r < c->nranks; ++r) {
-    q.pflags[r] = (unsigned long long*)c->peer_base[r];
-    q.pmbox[r] = (double*)((char*)c->peer_base[r] + kFlagBytes);
-  }
-  q.lflags = (unsigned long long*)c->xbuf;
+  for (int r = 0; r < c->nranks; ++r) q.pmbox[r] = (double*)((char*)c->peer_base[r] + kFlagBytes);
   q.lmbox = (double*)((char*)c->xbuf + kFlagBytes);
   c->ar_last += q.nxchg;
   c->ar_total += q.nxchg;
@@ -796,7 +792,8 @@ static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant,
 static int fused_setup(aa_ctx* c) {
   // Any failure here leaves the handle usable with ncclAllReduce (not sticky).
   if (c->nranks > MAX_RANKS || !nccl().AllGather) return AA_ERR_ARG;
-  const size_t bytes = kFlagBytes + (size_t)2 * c->nranks * LRED * sizeof(double);
+  // mailbox: [seq parity][source rank][LRED words][2 tagged halves] of 8 bytes (low-latency protocol)
+  const size_t bytes = kFlagBytes + (size_t)2 * c->nranks * LRED * 2 * sizeof(unsigned long long);
   char* dh = nullptr;
   std::vector<cudaIpcMemHandle_t> all(c->nranks);
   cudaIpcMemHandle_t mine;
