@@ -365,6 +365,10 @@ def main():
             outh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
             dh, bh = d.cpu(), b.cpu()
             xh.copy_(x.cpu())
+            # one untimed call: aa_step_host allocates its device staging buffers on first use
+            torch.addcmul(bh, dh, xh, out=gh)
+            s.step_host(xh, gh, outh)
+            xh, outh = outh, xh
             t_e = []
             for _ in range(nh):
                 torch.addcmul(bh, dh, xh, out=gh)    # caller's G on the host (untimed)
