@@ -235,7 +235,7 @@ constexpr int LDR = MMAX + 1;
 // rho = t * t^{-1/2}, c = a t^{-1/2}, s = b t^{-1/2} with t = a^2 + b^2 after an exact
 // power-of-two scaling (one MUFU-seeded rsqrt instead of sqrt + reciprocal, no branches).
 template <int LD>
-__device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn) {
+__device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn, int* progress = nullptr) {
   const int lane = threadIdx.x & 31;
   const int nc = mold - 1;  // columns of the Hessenberg matrix
   const int l0 = lane, l1 = lane + 32;
@@ -275,6 +275,10 @@ __device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn) {
       R[j + j * LD] = rho;
       cs[j] = c;
       sn[j] = s;
+      if (progress) {   // publish rotation j to a consumer warp (k3_rotate_sym)
+        __threadfence_block();
+        *reinterpret_cast<volatile int*>(progress) = j + 1;
+      }
     }
     h20 = n20;
     h21 = n21;
@@ -288,12 +292,22 @@ __device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn) {
 // indices <= P-2 are then W^T S W restricted to them (rotation P-1 would only touch row /
 // column P-1).  One pass per rotation: lane i (i != j, j+1) rotates (S[i][j], S[i][j+1]) and
 // writes both symmetric copies; one lane updates the 2 x 2 diagonal block in closed form.
+// With progress != nullptr the rotations are consumed as another warp publishes them.
 template <int LDS>
-__device__ void k3_rotate_sym(double* S, int P, const double* cs, const double* sn) {
+__device__ void k3_rotate_sym(double* S, int P, const double* cs, const double* sn,
+                              const int* progress = nullptr) {
   const int lane = threadIdx.x & 31;
   const int i0 = lane, i1 = lane + 32;
   for (int j = 0; j + 1 < P; ++j) {
-    const double c = cs[j], s = sn[j];
+    if (progress) {   // rotation j is produced by another warp (k3_givens_delete)
+      if (lane == 0)
+        while (*reinterpret_cast<const volatile int*>(progress) <= j) {
+        }
+      __syncwarp();
+      __threadfence_block();
+    }
+    const double c = *reinterpret_cast<const volatile double*>(cs + j);
+    const double s = *reinterpret_cast<const volatile double*>(sn + j);
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
     const bool u0 = i0 < P && i0 != j && i0 != j + 1, u1 = i1 < P && i1 != j && i1 != j + 1;
     if (u0) { a0 = S[i0 + j * LDS]; b0 = S[i0 + (j + 1) * LDS]; }

@@ -50,7 +50,7 @@ struct HeadArea {
   double redw[NWARP][4];
   int lcol[MMAX + 2];
   int rcol[4];
-  int na, nr, is_last, pad;
+  int na, nr, is_last, gdone;   // gdone: Givens rotations published (K4, ICWY SMALL)
 };
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -65,6 +65,9 @@ constexpr size_t SCR_V = SCR_TW + MMAX * MMAX;
 constexpr size_t SCR_R0 = SCR_V + 4 * MMAX;
 constexpr size_t SCR_RF = SCR_R0 + LRED;
 __host__ __device__ constexpr size_t scratch_bytes() { return (SCR_RF + 8) * sizeof(double); }
+// K4 with ICWY SMALL: the symmetric S of k4_tdel (m x LDR) after the scratch
+constexpr size_t SCR_S = SCR_RF + 8;
+__host__ __device__ constexpr size_t scratch_bytes_tdel(int m) { return (SCR_S + (size_t)m * LDR) * sizeof(double); }
 
 __device__ __forceinline__ double cur_scale(const KParams& p, int j) {
   // scale of stored Q column j as seen after this step's K1: rotated columns (QRDelete)
@@ -251,7 +254,8 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
   __syncwarp();
   // QRDelete of the new R, in place in shared memory, then R' and the rotations to Fo
   if (K >= 1) {
-    k3_givens_delete<LDR>(Rw, K, H.cs, H.sn);
+    k3_givens_delete<LDR>(Rw, K, H.cs, H.sn,
+                          (p.variant == V_ICWY && p.icwy_merged == 2) ? &H.gdone : nullptr);
     for (int j = 0; j < mm; ++j)
       for (int i = lane; i < mm; i += 32)
         Fo.Rdel[i + j * MMAX] = (i <= j && j < K - 1) ? Rw[i + j * LDR] : 0.0;
@@ -260,23 +264,23 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
       Fo.sn[j] = H.sn[j];
     }
     __syncwarp();
-    if (p.variant == V_ICWY && p.icwy_merged == 2) k4_tdel(p, H, scratch, Fo, K);
   }
   if (lane == 0) Fo.has_del = 1;
   __syncwarp();
 }
 
 // ICWY_DELETE = SMALL (variant, not in the paper, A6b):
-// the next QRDelete replaces Q by Q' = Q W (W = the rotations just computed, applied to
-// columns), so the post-delete Gram is W^T S W with S = T + T^T - I from the P = K-1 known
-// rows of T (Tw).  S is rotated two-sided in shared memory (Rw's area, leading dimension
-// MMAX+1 against bank conflicts): rotation j mixes columns then rows j, j+1; rotations
+// the next QRDelete replaces Q by Q' = Q W (W = the rotations warp 0 is computing, applied
+// to columns), so the post-delete Gram is W^T S W with S = T + T^T - I from the P = K-1
+// known rows of T (Tw).  Run by warp 1 of CTA 0 concurrently with warp 0's head and
+// QRDelete: S is built in its own shared region (leading dimension MMAX+1 against bank
+// conflicts) and rotated two-sided as each rotation is published (H.gdone); rotations
 // 0..P-2 fix every entry with both indices <= P-2, which are the rows the next step reads.
 __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K) {
   constexpr int LD = MMAX + 1;
   const int lane = threadIdx.x & 31;
   const double* Tw = scratch + SCR_TW;
-  double* S = scratch;   // Rw's area (R_new written, QRDelete done): MMAX x LD
+  double* S = scratch + SCR_S;   // own region (warp 0 still uses Rw for the QRDelete)
   const int P = K - 1;
   for (int j = 0; j < P; ++j)
     for (int i = j + lane; i < P; i += 32) {
@@ -285,7 +289,7 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
       S[j + i * LD] = v;
     }
   __syncwarp();
-  k3_rotate_sym<LD>(S, P, H.cs, H.sn);
+  k3_rotate_sym<LD>(S, P, H.cs, H.sn, &H.gdone);
   const int mm = p.m;
   for (int j = 0; j < mm; ++j)
     for (int i = lane; i < mm; i += 32)
@@ -557,6 +561,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   K4Head hd{};
   if (blockIdx.x == 0) AA_TL(0);
   if constexpr (OP == OP_K4 || OP == OP_K2_ICWY) {
+    if (OP == OP_K4 && tid == 0) H.gdone = 0;
     stage_small<OP>(p, scratch);
     __syncthreads();
   }
@@ -566,6 +571,10 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       hd = k4_head(p, H, scratch);
       if (blockIdx.x == 0) AA_TL(8);
       if (blockIdx.x == 0) k4_write_next(p, H, scratch, hd);
+    } else if (warp == 1 && blockIdx.x == 0 && p.variant == V_ICWY && p.icwy_merged == 2) {
+      // ICWY SMALL: the post-delete T, rotated as warp 0 publishes the Givens rotations
+      const int K = (p.flags & F_DELETE_ONLY) ? p.k : p.k + 1;
+      if (K >= 1) k4_tdel(p, H, scratch, p.st->f[p.ver ^ 1], K);
     }
   } else {
     if (warp == 0) op_head<OP>(p, H, scratch);

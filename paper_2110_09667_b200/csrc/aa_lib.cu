@@ -310,7 +310,9 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
     p.tm[b] = *m;
   }
   const size_t stage_bytes = (size_t)stages * align_up((size_t)nin * tr, 16) * sizeof(double);
-  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scratch_bytes());
+  const size_t scr = (OP == OP_K4 && p.variant == V_ICWY && p.icwy_merged == 2) ? scratch_bytes_tdel(p.m)
+                                                                                 : scratch_bytes();
+  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
   static size_t attr_set = 0;
   if (smem > attr_set) {
     CUDA_TRY(c, cudaFuncSetAttribute(aa_stream_kernel<OP, NCW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
