@@ -58,6 +58,7 @@ struct SmallState {
   // ---- scalar tail (aa_stats copies only this part)
   double dx2_local;          // this rank's ||x_{i+1} - x_i||^2 from the last update
   double dx2_global;         // CONV_NORM = IMMEDIATE: the same, summed over ranks by aa_step
+  double dx2_acc;            // chunked K4: ||x_{i+1} - x_i||^2 accumulated over row chunks
   double f2;                 // ||f_i||^2 (global) of the last step
   double rratio_min;         // min R_kk / ||Delta f||
   double last_rkk;
@@ -113,6 +114,9 @@ struct alignas(64) KParams {
   int red_slot;     // slot this kernel writes
   int words;        // words this kernel reduces
   int red_words0;   // words of reduction slot 0 the heads stage into shared memory
+  long long rbeg;   // first row of this launch (rows [rbeg, n)); 0 except chunked aa_step_host
+  int chunk_first;  // first / last row-chunk launch of this op in the step (both 1 unchunked):
+  int chunk_last;   // reductions accumulate over chunks; side effects happen once
   int pre_cta;      // K4 at small n: CTA 0 only writes the next factors + QRDelete precompute
                     // (no tiles); tiles go to CTAs 1..gridDim-1
   unsigned long long* tl;   // test-only phase timeline (CTA 0 / last CTA, %globaltimer ns), or null

@@ -551,10 +551,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   // then let the next kernel start launching (it waits the same way)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const long long n = p.n;
+  const long long n = p.n;          // rows [rbeg, n) are this launch's
+  const long long rbeg = p.rbeg;
   const int TR = p.tr, NS = p.stages;
   const size_t stage_words = align_up((size_t)p.nin * TR, 16);
-  const long long ntiles = (n + TR - 1) / TR;
+  const long long ntiles = (n > rbeg) ? (n - rbeg + TR - 1) / TR : 0;
   const int k = p.k;
   const int vb = p.vb;
 
@@ -570,8 +571,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     if (warp == 0) {
       hd = k4_head(p, H, scratch);
       if (blockIdx.x == 0) AA_TL(8);
-      if (blockIdx.x == 0) k4_write_next(p, H, scratch, hd);
-    } else if (warp == 1 && blockIdx.x == 0 && p.variant == V_ICWY && p.icwy_merged == 2) {
+      if (blockIdx.x == 0 && p.chunk_first) k4_write_next(p, H, scratch, hd);
+    } else if (warp == 1 && blockIdx.x == 0 && p.chunk_first && p.variant == V_ICWY && p.icwy_merged == 2) {
       // ICWY SMALL: the post-delete T, rotated as warp 0 publishes the Givens rotations
       const int K = (p.flags & F_DELETE_ONLY) ? p.k : p.k + 1;
       if (K >= 1) k4_tdel(p, H, scratch, p.st->f[p.ver ^ 1], K);
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     fence_proxy_async();
     for (int s = 0; s < NS && s < my_count; ++s) {
       const long long t = tb + (long long)s * tg;
-      const long long r0 = t * TR;
+      const long long r0 = rbeg + t * TR;
       issue_tile_part(p, stage0 + s * stage_words, &bars[s], r0, (int)min((long long)TR, n - r0), warp);
     }
   }
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     const int sidx = (int)(it % NS);
     const uint32_t par = (uint32_t)((it / NS) & 1);
     const long long tile = tb + it * tg;
-    const long long row0 = tile * TR;
+    const long long row0 = rbeg + tile * TR;
     const int rows = (int)min((long long)TR, n - row0);
     double* S = stage0 + sidx * stage_words;
     mbar_wait(&bars[sidx], par);
@@ -691,10 +692,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
             S[(size_t)vb * TR + r] = f;
             S[(size_t)(vb + 1) * TR + r] = df;
           }
-        } else if (!del_only) {
-          // Q block rows past n are zero-filled by the tensor copy
-          S[(size_t)vb * TR + r] = 0.0;
-          S[(size_t)(vb + 1) * TR + r] = 0.0;
+        } else {
+          // rows past this launch's range: the tensor copy zero-fills rows past n, but a
+          // row-chunked launch (aa_step_host) ends mid-vector, where the staged rows hold the
+          // next chunk's data -- zero them so the multi-dot and the Gram see only this range
+          for (int j = 0; j < p.c_in; ++j) S[(size_t)j * TR + r] = 0.0;
+          if (!del_only) {
+            S[(size_t)vb * TR + r] = 0.0;
+            S[(size_t)(vb + 1) * TR + r] = 0.0;
+          }
         }
       } else if constexpr (OP == OP_K2_ICWY || OP == OP_K2B_CGS2) {
         // ICWY: Alg. 4 l.5  Delta f - Q (T^{-1} r);  CGS-2: Alg. 5 l.4  y - Q z
@@ -833,7 +839,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     if (lane == 0 && it + NS < my_count) {
       fence_proxy_async();
       const long long t2 = tb + (it + NS) * tg;
-      const long long r2 = t2 * TR;
+      const long long r2 = rbeg + t2 * TR;
       issue_tile_part(p, S, &bars[sidx], r2, (int)min((long long)TR, n - r2), warp);
     }
   }
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           }
         }
       }
-      if (tid == 0) mypart[2] = (blockIdx.x == 0 && !(p.flags & F_EXT_DF)) ? p.st->dx2_local : 0.0;
+      if (tid == 0) mypart[2] = (blockIdx.x == 0 && p.chunk_first && !(p.flags & F_EXT_DF)) ? p.st->dx2_local : 0.0;
     }
     if constexpr (GRAM) {
       if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, del_only ? 1 : 0, L.off_x, L.off_gram);
@@ -929,6 +935,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   for (int w = tid; w < p.words; w += NT) {
     double s = 0.0;
     for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(p.part + (size_t)b * LRED + w);
+    // row-chunked launches (aa_step_host) add to the previous chunks' sums, in chunk order
+    if (!p.chunk_first) s += (OP == OP_K4) ? (w == 0 ? p.st->dx2_acc : 0.0) : outv[w];
     outv[w] = s;
   }
   __syncthreads();
@@ -936,8 +944,9 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     for (int e = 0; e < p.nxchg; ++e) fused_exchange(p, outv + p.xoff[e], p.xcnt[e], p.seq0 + e);
   }
   if constexpr (OP == OP_K4) {
+    if (tid == 0 && !p.chunk_last) p.st->dx2_acc = outv[0];
     // run-time scalars (the factors were written by CTA 0 from its head)
-    if (tid == 0 && !(p.flags & F_DELETE_ONLY)) {
+    if (tid == 0 && p.chunk_last && !(p.flags & F_DELETE_ONLY)) {
       SmallState* st = p.st;
       hd = k4_scalars_head(p);
       st->last_rkk = hd.rkk;

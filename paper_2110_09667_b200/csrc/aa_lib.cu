@@ -94,6 +94,8 @@ struct aa_ctx {
   double beta = 1.0, eps_a = -1.0;
   int icwy_merged = 0, dcgs2_cond = 3, dcgs2_rscale = 0, profile = 0;
   int conv_norm = 0;   // AA_OPT_CONV_NORM: 0 lagged, 1 immediate, 2 off
+  cudaStream_t cstream = nullptr;                     // aa_step_host copy stream (lazy)
+  cudaEvent_t chunk_evH[8] = {}, chunk_evK[8] = {};
   // ledger
   int64_t logical[5] = {0, 0, 0, 0, 0}, logical_last[5] = {0, 0, 0, 0, 0};
   int64_t ar_total = 0;
@@ -513,8 +515,26 @@ KParams base_params(aa_ctx* c) {
   p.eps_a = c->eps_a;
   p.icwy_merged = c->icwy_merged;
   p.rscale = c->dcgs2_rscale;
+  p.rbeg = 0;
+  p.chunk_first = 1;
+  p.chunk_last = 1;
   return p;
 }
+
+// aa_step_host at large n: the PCIe copies are split into row chunks on a copy stream so
+// that K1 starts on the first chunk while the rest is still in flight, and x_{i+1} goes back
+// chunk by chunk behind K4.  Chunk boundaries are multiples of 1024 rows.
+constexpr int kMaxChunks = 8;
+constexpr int64_t kChunkMinRows = 4 << 20;
+struct ChunkPlan {
+  int nc = 0;
+  int64_t b[kMaxChunks + 1];
+  cudaStream_t cs = nullptr;
+  cudaEvent_t* evH = nullptr;   // chunk c of x_i, G(x_i) is on the device
+  cudaEvent_t* evK = nullptr;   // K4 has written chunk c of x_{i+1}
+  const double* dev_xn = nullptr;
+  double* host_xn = nullptr;
+};
 
 #define RET_IF(x)            \
   do {                       \
@@ -524,7 +544,8 @@ KParams base_params(aa_ctx* c) {
 
 // One QRAdd (with the fused QRDelete when the window is full) and, unless
 // commit_only, the LSP solve and the x update.  mode: 0 = aa_step, 1 = aa_test_qradd.
-int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const double* vext) {
+int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const double* vext,
+             const ChunkPlan* cp = nullptr) {
   const bool ext = vext != nullptr;
   const int V = c->variant;
   const bool recycle = (c->mi == c->m);
@@ -582,8 +603,23 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     } else {
       k1_ar[0] = 0; k1_ar[1] = L.words; k1_ar[2] = 0; k1_ar[3] = 0;
     }
-    plan_ar(c, q, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]);
-    RET_IF(launch_op<OP_K1>(c, q, in, 0));
+    if (!cp) {
+      plan_ar(c, q, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]);
+      RET_IF(launch_op<OP_K1>(c, q, in, 0));
+    } else {
+      // row chunks: each launch waits only for its own chunk's copies; the reduction slot
+      // accumulates over the chunks (in order); only the last one exchanges
+      for (int ci = 0; ci < cp->nc; ++ci) {
+        KParams qc = q;
+        qc.rbeg = cp->b[ci];
+        qc.n = cp->b[ci + 1];
+        qc.chunk_first = (ci == 0);
+        qc.chunk_last = (ci == cp->nc - 1);
+        if (qc.chunk_last) plan_ar(c, qc, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]);
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, cp->evH[ci], 0));
+        RET_IF(launch_op<OP_K1>(c, qc, in, 0));
+      }
+    }
   }
   RET_IF(post_ar(c, c->red, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]));
   // ---------------- K2: the rest of QRAdd
@@ -662,7 +698,24 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
       if (q.beta_on) in.vector(c->fp, false);
       q.x_out = xn;
     }
-    RET_IF(launch_op<OP_K4>(c, q, in, 2));
+    if (!cp || ext) {
+      RET_IF(launch_op<OP_K4>(c, q, in, 2));
+    } else {
+      // row chunks: x_{i+1} chunk c goes back to the host as soon as K4 has written it
+      for (int ci = 0; ci < cp->nc; ++ci) {
+        KParams qc = q;
+        qc.rbeg = cp->b[ci];
+        qc.n = cp->b[ci + 1];
+        qc.chunk_first = (ci == 0);
+        qc.chunk_last = (ci == cp->nc - 1);
+        RET_IF(launch_op<OP_K4>(c, qc, in, 2));
+        CUDA_TRY(c, cudaEventRecord(cp->evK[ci], c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(cp->cs, cp->evK[ci], 0));
+        const size_t off = (size_t)cp->b[ci], cnt = (size_t)(cp->b[ci + 1] - cp->b[ci]);
+        CUDA_TRY(c, cudaMemcpyAsync(cp->host_xn + off, cp->dev_xn + off, cnt * sizeof(double),
+                                    cudaMemcpyDeviceToHost, cp->cs));
+      }
+    }
   }
   // CONV_NORM = IMMEDIATE: ||x_{i+1} - x_i||^2 summed over ranks now (Alg. 1 l.8 every step)
   if (!ext && c->conv_norm == 1 && c->nranks > 1) {
@@ -687,6 +740,17 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   }
   for (int i = 0; i < 5; ++i) c->logical[i] += c->logical_last[i];
   return AA_OK;
+}
+
+// aa_step on the handle's staging buffers with the row-chunked K1 / K4 of aa_step_host
+int aa_step_chunked(aa_ctx* h, const ChunkPlan* cp) {
+  int rc;
+  {
+    EvScope ev(h, 4);
+    rc = run_step(h, h->hx, h->hg, h->hxn, nullptr, cp);
+  }
+  if (rc == AA_OK) h->iter++;
+  return rc;
 }
 
 int check_handle(aa_handle_t h) {
@@ -962,10 +1026,42 @@ int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x
       return AA_ERR_NOMEM;
     }
   }
-  CUDA_TRY(h, cudaMemcpyAsync(h->hx, x_i, vb, cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(h->hg, gx_i, vb, cudaMemcpyHostToDevice, h->stream));
-  RET_IF(aa_step(h, h->hx, h->hg, h->hxn));
-  CUDA_TRY(h, cudaMemcpyAsync(x_next, h->hxn, vb, cudaMemcpyDeviceToHost, h->stream));
+  if (h->n < kChunkMinRows || h->mi == 0) {
+    CUDA_TRY(h, cudaMemcpyAsync(h->hx, x_i, vb, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(h->hg, gx_i, vb, cudaMemcpyHostToDevice, h->stream));
+    RET_IF(aa_step(h, h->hx, h->hg, h->hxn));
+    CUDA_TRY(h, cudaMemcpyAsync(x_next, h->hxn, vb, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return AA_OK;
+  }
+  // large n: chunked copies overlapped with K1 (uploads) and K4 (downloads)
+  if (!h->cstream) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < kMaxChunks; ++i) {
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->chunk_evH[i], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->chunk_evK[i], cudaEventDisableTiming));
+    }
+  }
+  ChunkPlan cp;
+  cp.nc = kMaxChunks;
+  for (int i = 0; i <= cp.nc; ++i) cp.b[i] = (i == cp.nc) ? h->n : ((h->n * i / cp.nc) / 1024) * 1024;
+  cp.cs = h->cstream;
+  cp.evH = h->chunk_evH;
+  cp.evK = h->chunk_evK;
+  cp.dev_xn = h->hxn;
+  cp.host_xn = x_next;
+  // the copy stream must not overwrite the staging buffers before earlier work on the
+  // handle's stream has finished with them
+  CUDA_TRY(h, cudaEventRecord(h->chunk_evK[0], h->stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->cstream, h->chunk_evK[0], 0));
+  for (int ci = 0; ci < cp.nc; ++ci) {
+    const size_t off = (size_t)cp.b[ci], cnt = (size_t)(cp.b[ci + 1] - cp.b[ci]);
+    CUDA_TRY(h, cudaMemcpyAsync(h->hx + off, x_i + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->cstream));
+    CUDA_TRY(h, cudaMemcpyAsync(h->hg + off, gx_i + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->cstream));
+    CUDA_TRY(h, cudaEventRecord(h->chunk_evH[ci], h->cstream));
+  }
+  RET_IF(aa_step_chunked(h, &cp));
+  CUDA_TRY(h, cudaStreamSynchronize(h->cstream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return AA_OK;
 }
@@ -1141,6 +1237,13 @@ int aa_destroy(aa_handle_t h) {
     if (h->peer_base[r] && h->peer_base[r] != h->xbuf) cudaIpcCloseMemHandle(h->peer_base[r]);
   cudaFree(h->xbuf);
   cudaFree(h->tl);
+  if (h->cstream) {
+    cudaStreamDestroy(h->cstream);
+    for (int i = 0; i < 8; ++i) {
+      cudaEventDestroy(h->chunk_evH[i]);
+      cudaEventDestroy(h->chunk_evK[i]);
+    }
+  }
   if (h->comm && h->own_comm && nccl().ok) nccl().CommDestroy(h->comm);
   cudaFree(h->Q);
   cudaFree(h->DG);
@@ -1227,6 +1330,13 @@ int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384) {
   if (!enable && h->tl) {
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     cudaFree(h->tl);
+  if (h->cstream) {
+    cudaStreamDestroy(h->cstream);
+    for (int i = 0; i < 8; ++i) {
+      cudaEventDestroy(h->chunk_evH[i]);
+      cudaEventDestroy(h->chunk_evK[i]);
+    }
+  }
     h->tl = nullptr;
   }
   if (out384 && h->tl) {

@@ -1,0 +1,66 @@
+"""aa_step_host at large n (>= 4M rows) splits the PCIe copies into row chunks overlapped
+with row-chunked K1 / K4 launches whose reductions accumulate over the chunks.  It must
+follow the device path (aa_step) to rounding, for every variant, through start-up and
+recycle iterations, and match the oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from aa_inputs import problems  # noqa: E402
+from oracle import aa_variant  # noqa: E402
+from paper_2110_09667_b200 import aa  # noqa: E402
+
+N = 5_000_003   # > 4M rows (chunked), odd (ragged last tile and odd exact-vector tail)
+
+
+@pytest.fixture(scope="module")
+def prob():
+    d, b = problems.diagonal(N)
+    return d, b, torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+
+
+@pytest.mark.parametrize("variant", ["dcgs2", "icwy", "cgs2", "mgs", "icwy_small"])
+def test_step_host_chunked_matches_device(prob, variant):
+    d, b, dt, bt = prob
+    m, iters = 5, 12
+    base = "icwy" if variant == "icwy_small" else variant
+    opt = dict(icwy_delete="small") if variant == "icwy_small" else {}
+    stream = torch.cuda.current_stream()
+    dev = aa.AndersonSolver(N, m, base, stream=stream, **opt)
+    hst = aa.AndersonSolver(N, m, base, stream=stream, **opt)
+    x = torch.zeros(N, dtype=torch.float64, device="cuda")
+    xn = torch.empty_like(x)
+    dev.init(x, dt * x + bt, xn)
+    x, xn = xn, x
+    xh = torch.zeros(N, dtype=torch.float64).pin_memory()
+    gh = torch.empty(N, dtype=torch.float64).pin_memory()
+    oh = torch.empty(N, dtype=torch.float64).pin_memory()
+    x0 = torch.zeros(N, dtype=torch.float64, device="cuda")
+    x1 = torch.empty_like(x0)
+    hst.init(x0, dt * x0 + bt, x1)
+    xh.copy_(x1.cpu())
+    bh, dh = bt.cpu(), dt.cpu()
+    worst = 0.0
+    for i in range(iters):
+        dev.step(x, dt * x + bt, xn)
+        x, xn = xn, x
+        torch.addcmul(bh, dh, xh, out=gh)
+        hst.step_host(xh, gh, oh)
+        xh, oh = oh, xh
+        a = x.cpu().numpy()
+        worst = max(worst, float(np.linalg.norm(xh.numpy() - a) / np.linalg.norm(a)))
+    sd, sh = dev.stats(), hst.stats()
+    dev.close()
+    hst.close()
+    assert worst <= 1e-12, worst
+    assert abs(sd.f_norm - sh.f_norm) <= 1e-12 * sd.f_norm
+    assert abs(sd.dx_norm - sh.dx_norm) <= 1e-10 * sd.dx_norm + 1e-300
+    assert sd.logical == sh.logical
+    if variant == "dcgs2":   # and the oracle, once
+        o2 = aa_variant(lambda v: d * v + b, np.zeros(N), m, "dcgs2", iters, record_loo=False)
+        assert np.linalg.norm(xh.numpy() - o2.xs[-1]) <= 1e-10 * np.linalg.norm(o2.xs[-1])
