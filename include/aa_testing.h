@@ -42,11 +42,12 @@ int aa_fill_uniform(double* out_dev, int64_t n, int64_t offset, uint64_t seed, u
                     double lo, double hi, void* cuda_stream);
 
 /* Test-only phase timeline: enable = 1 allocates a 384-word device buffer; every kernel's
- * CTA 0 (slots op*16 + 0..5, K4 head sub-phases 8..11) and last CTA (slots 6, 7) record
+ * CTA 0 (slots op*16 + 0..5, K4 after its head: slot 8) and last CTA (slots 6, 7) record
  * %globaltimer (ns) at: entry, after staging, after the head, first tile ready, tiles done,
- * partials written, reduction begin, end; words 128 + slot hold clock64 at the same points;
- * words 256.. hold clock64 at each Givens step of K4's QRDelete precompute.
- * out384 (host, may be NULL) receives the buffer (synchronises). */
+ * partials written, reduction begin, end; words 128 + slot hold clock64 at the same points.
+ * out384 (host, may be NULL) receives the buffer (synchronises).  Enabled, the marks
+ * themselves lengthen short phases (timer reads and global stores on the critical path):
+ * use it to order phases, and ncu launch lists / PC sampling for durations. */
 int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384);
 
 /* Build-time facts: sm target, tile rows, stages, block size (for the report). */
