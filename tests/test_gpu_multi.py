@@ -58,3 +58,22 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
             assert ars[i - 1] == want, (variant, i, ars)
         assert r["gamma_identical_across_ranks"]
         assert r["loo"] < 1e-12
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("mode", ["fused", "nccl"])
+def test_multi_gpu_step_host_chunked(tmp_path, mode):
+    """aa_step_host at n_local > 4M rows (row-chunked K1 / K4, exchange in the last chunk)
+    follows aa_step on every rank, in both reduction modes, with the same allreduce count."""
+    world = min(torch.cuda.device_count(), 4)
+    out = tmp_path / "host.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
+           f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "_dist_host_worker.py"), str(out), mode]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    for rep in json.load(open(out)):
+        for variant, r in rep.items():
+            assert r["worst"] <= 1e-12, (variant, r)
+            assert r["ar_dev"] == r["ar_host"], (variant, r)
+            assert abs(r["f_dev"] - r["f_host"]) <= 1e-12 * r["f_dev"], (variant, r)
