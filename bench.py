@@ -167,7 +167,14 @@ def oracle_sample(m, variant, n_sample, steps, warmup, n_target):
         return out
 
     # run start-up + warmup + steps; the time between consecutive G calls is one AA
-    # iteration of the oracle (G itself excluded)
+    # iteration of the oracle (G itself excluded).  The oracle gets the host's cores even under
+    # torchrun (which sets OMP_NUM_THREADS=1 for every rank; only rank 0 runs this).
+    try:
+        from threadpoolctl import threadpool_limits
+        ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        limiter = threadpool_limits(limits=ncores)
+    except Exception:
+        limiter = None
     aa_variant(G_timed, np.zeros(n_sample), m, variant, m + warmup + steps + 1, record_x=False,
                record_loo=False)
     it_times = times[2 + m + warmup: 2 + m + warmup + steps]
@@ -177,6 +184,8 @@ def oracle_sample(m, variant, n_sample, steps, warmup, n_target):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
+    if limiter is not None:
+        limiter.unregister()
     return per_iter * (n_target / n_sample) * 1e6, cores, per_iter * 1e6
 
 
