@@ -364,3 +364,42 @@ def test_conv_norm_options():
     o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, "dcgs2", iters)
     for a, r in zip(lag.dx_norms, o2.dx_norms):
         assert abs(a - r) <= 1e-10 * r + 1e-15
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_output_may_alias_inputs(variant):
+    """aa.h: output vectors may alias inputs of the same call.  x_next = x_i (in place) and
+    x_next = G(x_i) must give bitwise the same iterates as a separate output buffer
+    (K4 stages each row of x_i and G(x_i) before writing that row of x_{i+1})."""
+    n, m, iters = 70001, 6, 14
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    stream = torch.cuda.current_stream()
+    runs = {}
+    for mode in ("separate", "in_place", "into_g"):
+        for beta in (1.0, 0.7):
+            s = aa.AndersonSolver(n, m, variant, stream=stream, beta=None if beta == 1.0 else beta)
+            x = torch.zeros(n, dtype=torch.float64, device="cuda")
+            x1 = torch.empty_like(x)
+            s.init(x, dt * x + bt, x1)
+            x = x1
+            xs = []
+            for _ in range(iters):
+                g = dt * x + bt
+                if mode == "separate":
+                    xn = torch.empty_like(x)
+                    s.step(x, g, xn)
+                    x = xn
+                elif mode == "in_place":
+                    s.step(x, g, x)
+                else:
+                    s.step(x, g, g)
+                    x = g
+                xs.append(x.clone())
+            s.close()
+            runs[(mode, beta)] = torch.stack(xs).cpu().numpy()
+    for beta in (1.0, 0.7):
+        ref = runs[("separate", beta)]
+        assert np.all(np.isfinite(ref))
+        for mode in ("in_place", "into_g"):
+            assert np.array_equal(runs[(mode, beta)], ref), (mode, beta)
