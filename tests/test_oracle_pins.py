@@ -200,6 +200,34 @@ def test_qradd_matches_householder(variant):
         assert per == want
 
 
+@pytest.mark.parametrize("opt", [dict(dcgs2_rscale=True), dict(dcgs2_cond=2)])
+def test_dcgs2_options_match_householder(opt):
+    """DCGS-2 with the consistent R update (reading A3) or reorthogonalising from m_i > 2
+    (reading A2) still reproduces LAPACK Householder QR at kappa <= 1e2; cond = 2 costs 2
+    reductions per add from the third column (the first two adds are unchanged)."""
+    for seed in range(5):
+        A = problems.ortho_test_matrix(300, 8, 1e2, seed=seed)
+        st, led, per = _build("dcgs2", A, **opt)
+        Qh, Rh = _signfix(*np.linalg.qr(A))
+        assert np.max(np.abs(st.R - Rh)) <= 1e-10 * np.max(np.abs(Rh))
+        assert np.max(np.abs(st.Q - Qh)) <= 1e-10
+        assert per == [1] + [2] * 7
+
+
+def test_dcgs2_rscale_keeps_the_factorisation_consistent():
+    """Reading A3 (SURVEY Pr5): at kappa = 1e6 the printed update R += s leaves F != QR at a
+    level far above rounding, while R += R_kk s keeps ||A - QR||/||A|| at rounding level;
+    the loss of orthogonality is the same class for both (the R update does not touch Q)."""
+    A = problems.ortho_test_matrix(1500, 30, 1e6, seed=2)
+    res = lambda st: np.linalg.norm(A - st.Q @ st.R) / np.linalg.norm(A)
+    st_v, _, _ = _build("dcgs2", A)
+    st_r, _, _ = _build("dcgs2", A, dcgs2_rscale=True)
+    assert res(st_r) <= 1e-14, res(st_r)
+    assert res(st_v) >= 1e3 * res(st_r), (res(st_v), res(st_r))
+    lv, lr = loss_of_orthogonality(st_v.Q), loss_of_orthogonality(st_r.Q)
+    assert lv == lr
+
+
 @pytest.mark.parametrize("kappa", [1e1, 1e3, 1e6, 1e9])
 def test_loss_of_orthogonality_classes(kappa):
     """S:211 with c = 100, n = 500, m = 20: MGS, ICWY <= c eps kappa (P:169, P:189);
