@@ -292,8 +292,9 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
     const long long nrows = p.n - p.rbeg;
     while (!skew && !vec_only && tr >= 512 && tr % 256 == 0 && ((nrows + tr - 1) / tr) * 2 <= c->sms) tr /= 2;
   }
-  // tuning override (tools only): AA_TILE="<op>:<tr>:<stages>[,<op>:<tr>:<stages>...]"
-  if (const char* ov = getenv("AA_TILE")) {
+  // tuning override (tools only): AA_TILE="<op>:<tr>:<stages>[,<op>:<tr>:<stages>...]", read once
+  static const char* const tile_override = getenv("AA_TILE");
+  if (const char* ov = tile_override) {
     const char* q = ov;
     while (*q) {
       int o, t, s, used = 0;
@@ -327,9 +328,21 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
                                      (int)std::max<size_t>(smem, 110 * 1024)));
     attr_set = std::max<size_t>(smem, 110 * 1024);
   }
-  int per_sm = 1;
-  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP, NCW, G>, NT, smem));
-  per_sm = std::max(1, std::min(per_sm, 2));
+  // resident CTAs per SM for this instance and shared-memory size (cached: the query costs
+  // host time on every launch otherwise, which matters at small n)
+  static size_t occ_smem[8];
+  static int occ_val[8], occ_n = 0;
+  int per_sm = 0;
+  for (int i = 0; i < occ_n; ++i)
+    if (occ_smem[i] == smem) per_sm = occ_val[i];
+  if (per_sm == 0) {
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP, NCW, G>, NT, smem));
+    per_sm = std::max(1, std::min(per_sm, 2));
+    if (occ_n < 8) {
+      occ_smem[occ_n] = smem;
+      occ_val[occ_n++] = per_sm;
+    }
+  }
   const long long ntiles = (p.n + p.tr - 1) / p.tr;
   long long grid = std::min<long long>(ntiles, (long long)c->sms * per_sm);
   if (grid < 1) grid = 1;
