@@ -27,6 +27,8 @@
  *    O(m^2) words, allocated once in aa_create.
  *  - aa_init / aa_step / aa_delete_oldest only ENQUEUE on the handle's stream
  *    and return without a host synchronisation.  aa_stats synchronises.
+ *  - A handle belongs to the CUDA device that was current at aa_create; call
+ *    it with that device current (one process per GPU is the intended use).
  *  - Host control flow depends only on (i, m_i, variant, options), all known
  *    on the host; no device->host transfer happens per iteration.
  *  - Errors: argument errors return immediately with no state change.  A CUDA

@@ -322,25 +322,28 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const size_t scr = (OP == OP_K4 && p.variant == V_ICWY && p.icwy_merged == 2) ? scratch_bytes_tdel(p.m)
                                                                                  : scratch_bytes();
   const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
-  static size_t attr_set = 0;
-  if (smem > attr_set) {
+  // per-device state of this instance (function attributes are set per device)
+  constexpr int kMaxDev = 16;
+  const int dev = (c->device >= 0 && c->device < kMaxDev) ? c->device : 0;
+  static size_t attr_set[kMaxDev] = {};
+  if (smem > attr_set[dev]) {
     CUDA_TRY(c, cudaFuncSetAttribute(aa_stream_kernel<OP, NCW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smem, 110 * 1024)));
-    attr_set = std::max<size_t>(smem, 110 * 1024);
+    attr_set[dev] = std::max<size_t>(smem, 110 * 1024);
   }
   // resident CTAs per SM for this instance and shared-memory size (cached: the query costs
   // host time on every launch otherwise, which matters at small n)
-  static size_t occ_smem[8];
-  static int occ_val[8], occ_n = 0;
+  static size_t occ_smem[kMaxDev][8];
+  static int occ_val[kMaxDev][8], occ_n[kMaxDev] = {};
   int per_sm = 0;
-  for (int i = 0; i < occ_n; ++i)
-    if (occ_smem[i] == smem) per_sm = occ_val[i];
+  for (int i = 0; i < occ_n[dev]; ++i)
+    if (occ_smem[dev][i] == smem) per_sm = occ_val[dev][i];
   if (per_sm == 0) {
     CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, aa_stream_kernel<OP, NCW, G>, NT, smem));
     per_sm = std::max(1, std::min(per_sm, 2));
-    if (occ_n < 8) {
-      occ_smem[occ_n] = smem;
-      occ_val[occ_n++] = per_sm;
+    if (occ_n[dev] < 8) {
+      occ_smem[dev][occ_n[dev]] = smem;
+      occ_val[dev][occ_n[dev]++] = per_sm;
     }
   }
   const long long ntiles = (p.n + p.tr - 1) / p.tr;
