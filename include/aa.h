@@ -162,7 +162,10 @@ int aa_set_option(aa_handle_t h, int opt, double val);
 int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out);
 
 /* One AA iteration (Alg. 1 l.3-7 with Alg. 2): given x_i and G(x_i) produce x_{i+1}.
- * QRDelete is fused in automatically when the window is full (m_i == m). */
+ * QRDelete is fused in automatically when the window is full (m_i == m).  The library
+ * asserts its reduction schedule: if a step issued a number of global reductions other than
+ * the paper's count (plus ICWY's separate delete reduction, A6, and the
+ * IMMEDIATE norm), it returns AA_ERR_STATE (sticky) and prints the two counts. */
 int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next);
 
 /* Same computation with HOST buffers (pinned or pageable): copies in, runs aa_step,

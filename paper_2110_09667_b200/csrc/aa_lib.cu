@@ -761,6 +761,20 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     c->logical_last[AA_PH_NORM] = (c->conv_norm == 2) ? 0 : 1;
   }
   for (int i = 0; i < 5; ++i) c->logical[i] += c->logical_last[i];
+  // the library asserts its schedule against the paper's count: the physical
+  // global reductions of this step are QRAdd's (the printed formula), plus ICWY's delete
+  // reduction when it is issued on its own and is non-empty (A6), plus the convergence norm
+  // when CONV_NORM = IMMEDIATE on several ranks; the LSP right-hand side and the lagged norm
+  // ride in these (A14, A15)
+  {
+    const int want = add + ((V == V_ICWY && gram && L.n_gram > 0 && !c->icwy_merged) ? 1 : 0) +
+                     ((!ext && c->conv_norm == 1 && c->nranks > 1) ? 1 : 0);
+    if (c->sp_last != want) {
+      fprintf(stderr, "libaa: schedule issued %d global reductions, the paper's count is %d (variant %d, k %d)\n",
+              c->sp_last, want, V, k);
+      return fail(c, AA_ERR_STATE);
+    }
+  }
   return AA_OK;
 }
 
