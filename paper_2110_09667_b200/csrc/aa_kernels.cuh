@@ -497,7 +497,8 @@ __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned lo
   const int tid = threadIdx.x;
   const int R = p.nranks;
   const int par = (int)(seq & 1ull);
-  const unsigned long long tag = (seq & 0xffffffffull) << 32;
+  // 32-bit tag in 1 .. 2^32-1 (never 0, the value of a mailbox word never written)
+  const unsigned long long tag = (((seq - 1ull) % 0xffffffffull) + 1ull) << 32;
   for (int i = tid; i < cnt * R; i += NT) {
     const int q = i / cnt, w = i - q * cnt;
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v[w]);
