@@ -279,7 +279,14 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   if (OP == OP_K1 && !skew && nin < 20 && regs <= 128)
     // K1 with few columns: keep two CTAs per SM (16 warps hide the rotation chain)
     k1_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, c->max_tr_blocks, &tr, &stages) && tr >= 256;
-  if (!k1_two)
+  // CGS-2's K2a (phase B dots the y that phase A just produced, so a tile's two phases
+  // serialise): two CTAs per SM overlap them -- the tallest tile, up to 1024 rows, whose
+  // 2-stage ring lets two CTAs share an SM (sweeps: m = 20 256 rows, K2 5.34 -> 5.05 ms;
+  // m = 5 1024 rows, 1.97 -> 1.74 ms)
+  bool k2a_two = false;
+  if (OP == OP_K2A_CGS2 && !skew && regs <= 128)
+    k2a_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, 1024, &tr, &stages) && tr >= 256;
+  if (!k1_two && !k2a_two)
     choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, vec_only ? 1024 : c->max_tr_blocks, &tr, &stages);
   if (OP != OP_K1) {
     const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
