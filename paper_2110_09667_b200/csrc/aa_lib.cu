@@ -286,8 +286,12 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   bool k2a_two = false;
   if (OP == OP_K2A_CGS2 && !skew && regs <= 128)
     k2a_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, 1024, &tr, &stages) && tr >= 256;
+  // the projection kernels (K2 ICWY / DCGS-2, CGS-2's K2b) stream best with tiles up to 1024
+  // rows when few columns let a 2-stage ring fit (m = 5 / 10: K2 3-6 % faster; m >= 20 falls
+  // back to 512 rows by itself); K1 and K4 keep 512
+  const bool tall = vec_only || OP == OP_K2_ICWY || OP == OP_K2_DCGS2 || OP == OP_K2B_CGS2;
   if (!k1_two && !k2a_two)
-    choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, vec_only ? 1024 : c->max_tr_blocks, &tr, &stages);
+    choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, tall ? 1024 : c->max_tr_blocks, &tr, &stages);
   if (OP != OP_K1) {
     const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
     const size_t budget = (regs <= 128 && 2 * sb <= 104 * 1024) ? 104 * 1024 : 0;
