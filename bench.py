@@ -484,7 +484,8 @@ def main():
             "bytes_per_launch": k1b, "k1_ms": head["k1_ms"],
             # K1 reads 24 and writes 23 columns per row; a plain streaming microbenchmark of that
             # exact read/write mix (tools/rw_bench.cu) sustains 6.66 TB/s on B200
-            "rw_mix_ceiling_gbs": 6660.0, "frac_of_rw_mix_ceiling": achieved / 6660.0,
+            "rw_mix_ceiling_gbs": 6660.0 if args.m == 20 else None,
+            "frac_of_rw_mix_ceiling": achieved / 6660.0 if args.m == 20 else None,
             "step_bytes": step_bytes(args.variant, args.m, V),
             "step_frac": step_bytes(args.variant, args.m, V) / (head["ms_per_step"] * 1e-3) / (peak * 1e9),
             "k1_share_of_step": head["k1_ms"] / head["ms_per_step"]}
