@@ -39,6 +39,24 @@
  *    the same m / variant / options.  n_local may differ per rank (contiguous
  *    row blocks).
  *  - Handles are not thread-safe.  One handle per solve.
+ *
+ * BREAKDOWN (reading A12: the paper is silent on linear dependence in the window; SPEC
+ * S:145).  K4 tests the step's new column on the
+ * device: R_kk <= eps_a ||Delta f_{i-1}|| (eps_a = 10 eps sqrt(n_global) by default,
+ * n_global = the sum of every rank's n_local, so all ranks use the same threshold; the two
+ * norms are global reduction results, so all ranks take the same decision).  Then:
+ *  - that step degrades to gamma = 0: x_{i+1} = G(x_i) exactly (Alg. 1 l.1 restarted from
+ *    x_i; no damping term), and a flag is set that stays set until aa_reset or aa_init;
+ *  - while the flag is set every further aa_step also degrades to x_{i+1} = G(x_i) (the
+ *    window holding the dependent column is never used again; it keeps f_{i-1}, G(x_{i-1})
+ *    current, so aa_reset restarts Alg. 2 at the right place);
+ *  - the flag is surfaced by aa_stats (returns AA_ERR_BREAKDOWN with the stats filled)
+ *    and, with nranks == 1, at aa_step entry: a mapped pinned word written by K4 is polled
+ *    without blocking and aa_step returns AA_ERR_BREAKDOWN without enqueuing anything
+ *    (steps enqueued before K4 ran are the degraded steps above);
+ *  - the caller applies SPEC's policy: aa_reset once; a breakdown again on the first
+ *    step after the reset is a hard error.  The handle is not failed by a breakdown.
+ *  - AA_OPT_BREAKDOWN_EPS = 0 disables the test except for R_kk = 0 or NaN (stress runs).
  */
 #ifndef AA_H
 #define AA_H
@@ -66,8 +84,9 @@ enum aa_status {
     AA_ERR_CUDA = 3,       /* CUDA runtime failure (sticky)                              */
     AA_ERR_NCCL = 4,       /* NCCL failure or NCCL library unavailable (sticky)         */
     AA_ERR_NOMEM = 5,      /* device allocation failed in aa_create                     */
-    AA_ERR_BREAKDOWN = 6   /* reported by aa_stats: a new column was (numerically)
-                              linearly dependent (R_kk <= eps_a ||Delta f||, reading A12) */
+    AA_ERR_BREAKDOWN = 6   /* a new column was (numerically) linearly dependent:
+                              R_kk <= eps_a ||Delta f|| (or NaN), reading A12 (S:145,
+                              S:215).  NOT sticky-failed: see "BREAKDOWN" below          */
 };
 
 /* Options for aa_set_option (call after aa_create, before aa_init). */
@@ -132,8 +151,8 @@ struct aa_stats {
     double dx_norm;            /* ||x_{i+1} - x_i||_2 of the last step (global)             */
     double r_ratio_min;        /* min over the run of R_kk / ||Delta f|| (breakdown margin)  */
     double loo;                /* ||I - Q^T Q||_F if AA_STATS_LOO, else -1                  */
-    int32_t breakdown;         /* sticky breakdown flag                                     */
-    int32_t pad1;
+    int32_t breakdown;         /* breakdown flag, sticky until aa_reset / aa_init           */
+    int32_t breakdown_count;   /* steps that broke down since aa_init                       */
 };
 
 /* NCCL rendezvous: rank 0 calls this, broadcasts the 128 bytes (e.g. with
@@ -167,6 +186,8 @@ int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out);
  * the paper's count (plus ICWY's separate delete reduction, A6, and the
  * IMMEDIATE norm), it returns AA_ERR_STATE (sticky) and prints the two counts. */
 int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next);
+/* (aa_step returns AA_ERR_BREAKDOWN, enqueuing nothing, when nranks == 1 and an earlier step
+ * broke down and aa_reset has not been called since; see BREAKDOWN above.) */
 
 /* Same computation with HOST buffers (pinned or pageable): copies in, runs aa_step,
  * copies x_next back and synchronises.  For end-to-end measurement. */
@@ -179,11 +200,15 @@ int aa_step_host(aa_handle_t h, const double* x_i_host, const double* gx_i_host,
 int aa_delete_oldest(aa_handle_t h);
 
 /* Synchronises the stream and reports counters; see struct aa_stats.  Returns
- * AA_ERR_BREAKDOWN if the sticky breakdown flag is set (stats still filled). */
+ * AA_ERR_BREAKDOWN if the breakdown flag is set (stats still filled).  Collective when
+ * nranks > 1: every call does ONE allreduce of {this rank's lagged ||x_{i+1}-x_i||^2
+ * partial, an error flag}, so the ranks agree: if any rank's handle failed (e.g. a fused
+ * exchange timed out) every rank returns AA_ERR_NCCL.  AA_STATS_LOO adds one more. */
 int aa_stats(aa_handle_t h, struct aa_stats* out, int flags);
 
-/* Empty the window (restart policy after a breakdown).  The next aa_step
- * behaves like Alg. 2's i = 1 branch. */
+/* Empty the window and clear the breakdown flag (restart policy after a breakdown,
+ * S:256).  The next aa_step behaves like Alg. 2's i = 1 branch with
+ * Delta f = f_i - f_{i-1} of the last two iterates.  Synchronises the stream. */
 int aa_reset(aa_handle_t h);
 
 int aa_destroy(aa_handle_t h);

@@ -10,8 +10,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .qr import (Ledger, QRState, Reducer, back_substitution, icwy_rebuild_T, icwy_update_T_small,
-                 loss_of_orthogonality, lsp_solve, qradd, qrdelete_givens)
+from .qr import (Ledger, QRState, Reducer, _breakdown_check, back_substitution, icwy_rebuild_T,
+                 icwy_update_T_small, loss_of_orthogonality, lsp_solve, qradd, qrdelete_givens)
 
 
 @dataclass
@@ -27,6 +27,7 @@ class AAResult:
     loo: list = field(default_factory=list)       # ||I - Q^T Q||_F after the update (O2)
     ledgers: list = field(default_factory=list)   # cumulative ledger snapshot after each iteration
     breakdown: list = field(default_factory=list)
+    rratio: list = field(default_factory=list)    # R_kk / ||Delta f|| of the step's QRAdd (O2)
     x1: np.ndarray | None = None
 
 
@@ -85,7 +86,8 @@ def aa_definition(G, x0: np.ndarray, m: int, max_iters: int, tol: float = 0.0,
 def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: float = 0.0,
                beta: float = 1.0, shards: int = 1, dcgs2_cond: int = 3,
                dcgs2_rscale: bool = False, record_x: bool = True, record_loo: bool = True,
-               dfs_override=None, icwy_delete: str = "rebuild") -> AAResult:
+               dfs_override=None, icwy_delete: str = "rebuild", breakdown: str = "record",
+               breakdown_eps: float | None = None) -> AAResult:
     """O2: Alg. 1 + Alg. 2 with the paper's incremental QR (variant in mgs/icwy/cgs2/dcgs2).
 
     ``icwy_delete``: "rebuild" = the paper's T update after QRDelete, one reduction
@@ -93,7 +95,19 @@ def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: flo
     (not in the paper).
     Ledger phases: qradd (Algs. 2 l.2, 3-6), qrdelete (ICWY rebuild),
     lsp_rhs (Alg. 2 l.9), norm_check (Alg. 1 l.8).
-    Damping (reading A13): x_{i+1} = g_i - G_i gamma - (1-beta)(f_i - Q (Q^T f_i))."""
+    Damping (reading A13): x_{i+1} = g_i - G_i gamma - (1-beta)(f_i - Q (Q^T f_i)).
+
+    ``breakdown`` (reading A12; the paper is silent on linear dependence): a QRAdd breaks
+    down when its new R_kk <= eps_a ||Delta f|| (eps_a = 10 eps sqrt(n) unless
+    ``breakdown_eps`` is given).  "record" only records it (res.breakdown) and carries on
+    with the factorisation as computed (stress runs, config 5).  "restart" is SPEC's policy
+     as SURVEY.md §8(b) assigns it to the library and its caller: the
+    breaking step degrades to gamma = 0, i.e. x_{i+1} = G(x_i) (Alg. 1 l.1 restarted from
+    x_i), the window is emptied, the next iteration takes Alg. 2's i = 1 branch with
+    Delta f = f_{i+1} - f_i; a breakdown on that first step after a restart is a hard error
+    (res.hard_error, the run stops)."""
+    if breakdown not in ("record", "restart"):
+        raise ValueError(f"unknown breakdown policy {breakdown!r}")
     x0 = np.asarray(x0, dtype=np.float64)
     n = x0.shape[0]
     red = Reducer(shards)
@@ -103,22 +117,27 @@ def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: flo
     f_prev, g_prev = g - x0, g
     x = np.array(g, copy=True)
     res = AAResult(x=x, iters=0, converged=False, x1=x.copy())
+    st.eps_a = breakdown_eps
+    res.hard_error = False
     dG: deque = deque()
+    restarted = False                           # the previous step broke down (policy "restart")
     for i in range(1, max_iters + 1):
         g = G(x)                                # Alg. 1 l.3
         f = g - x
         df = f - f_prev                         # l.5  Delta f_{i-1}
         dg = g - g_prev                         # l.4  Delta g_{i-1}
         st.breakdown = False
-        if i == 1:                              # Alg. 2 l.1-2
+        if st.mi == 0:                          # Alg. 2 l.1-2 (i = 1, or the first step after a restart)
             r00 = red.norm(df)
             led.sync("qradd")
+            _breakdown_check(st, r00, r00)      # Delta f = 0: R_00 = 0 (A12)
             st.R[0, 0] = r00
-            st.Q[:, 0] = df / r00
+            with np.errstate(invalid="ignore", divide="ignore"):
+                st.Q[:, 0] = df / r00
             st.T[0, 0] = 1.0
             st.mi = 1
         else:
-            if i > m:                           # Alg. 2 l.4-5  QRDelete
+            if st.mi == m:                      # Alg. 2 l.4-5  QRDelete (i > m)
                 rots = qrdelete_givens(st)
                 dG.popleft()
                 if variant == "icwy":
@@ -129,18 +148,25 @@ def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: flo
             qradd(variant, st, df, led, red, dcgs2_cond, dcgs2_rscale)   # Alg. 2 l.7
         dG.append(dg)
         k = st.mi
-        gamma = lsp_solve(st, f, led, red)      # Alg. 2 l.9
-        Gm = np.stack(dG, axis=1)
-        x_new = g - Gm @ gamma                  # Alg. 1 l.7
-        if beta != 1.0:
-            c = st.Q[:, :k].T @ f
-            x_new = x_new - (1.0 - beta) * (f - st.Q[:, :k] @ c)
+        if breakdown == "restart" and st.breakdown:
+            # the step degrades to gamma = 0: x_{i+1} = G(x_i); the dependent column is not kept
+            led.sync("lsp_rhs")                 # Q^T f_i rode in the step's reductions all the same
+            gamma = np.zeros(k)
+            x_new = np.array(g, copy=True)
+        else:
+            gamma = lsp_solve(st, f, led, red)  # Alg. 2 l.9
+            Gm = np.stack(dG, axis=1)
+            x_new = g - Gm @ gamma              # Alg. 1 l.7
+            if beta != 1.0:
+                c = st.Q[:, :k].T @ f
+                x_new = x_new - (1.0 - beta) * (f - st.Q[:, :k] @ c)
         dx = red.norm(x_new - x)                # Alg. 1 l.8
         led.sync("norm_check")
         res.f_norms.append(red.norm(f))
         res.dx_norms.append(dx)
         res.gammas.append(gamma)
         res.breakdown.append(st.breakdown)
+        res.rratio.append(st.last_ratio)
         if record_loo:
             res.loo.append(loss_of_orthogonality(st.Q[:, :k]))
         res.ledgers.append(led.snapshot())
@@ -149,6 +175,16 @@ def aa_variant(G, x0: np.ndarray, m: int, variant: str, max_iters: int, tol: flo
         x = x_new
         f_prev, g_prev = f, g
         res.iters = i
+        if breakdown == "restart" and st.breakdown:
+            if restarted:                       # second consecutive breakdown
+                res.hard_error = True
+                break
+            restarted = True
+            st = QRState(n, m)                  # empty the window (aa_reset)
+            st.eps_a = breakdown_eps
+            dG.clear()
+        else:
+            restarted = False
         if dx < tol:
             res.converged = True
             break

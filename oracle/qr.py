@@ -103,6 +103,7 @@ class QRState:
         self.T = np.zeros((m, m))
         self.mi = 0
         self.breakdown = False
+        self.eps_a = None        # breakdown threshold; None = 10 eps sqrt(n) (reading A12)
 
 
 # --------------------------------------------------------------------------------------
@@ -137,10 +138,18 @@ def loss_of_orthogonality(Q: np.ndarray) -> float:
     return float(np.linalg.norm(np.eye(k) - Q.T @ Q, "fro"))
 
 
+def breakdown_eps_default(n: int) -> float:
+    """eps_a = 10 eps sqrt(n), n the GLOBAL vector length (reading A12)."""
+    return 10.0 * EPS * math.sqrt(n)
+
+
 def _breakdown_check(st: QRState, rkk: float, vnorm0: float) -> None:
-    """Reading A12 (paper silent): breakdown if R_kk <= 10 eps sqrt(n) ||v_orig||.
-    Recorded, not acted on (the caller decides)."""
-    if rkk <= 10.0 * EPS * math.sqrt(st.n) * vnorm0:
+    """Reading A12 (paper silent): breakdown if R_kk <= eps_a ||v_orig||,
+    v_orig the column before projection.  NaN counts as a breakdown (not R_kk > threshold).
+    Recorded here; the driver's policy acts on it (oracle.aa_variant ``breakdown``)."""
+    eps_a = st.eps_a if st.eps_a is not None else breakdown_eps_default(st.n)
+    st.last_ratio = rkk / vnorm0 if vnorm0 > 0.0 else 0.0
+    if not (rkk > eps_a * vnorm0):
         st.breakdown = True
 
 
@@ -154,7 +163,8 @@ def _normalise_new_column(st, v, k, led, red, vnorm0):
     led.sync("qradd")
     _breakdown_check(st, rkk, vnorm0)
     st.R[k, k] = rkk
-    st.Q[:, k] = v / rkk
+    with np.errstate(invalid="ignore", divide="ignore"):
+        st.Q[:, k] = v / rkk
     st.mi = k + 1
 
 

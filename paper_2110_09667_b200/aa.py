@@ -35,7 +35,7 @@ class AAStatsC(C.Structure):
                 ("allreduce_last", C.c_int32), ("pad0", C.c_int32), ("allreduce_total", C.c_int64),
                 ("logical_sync", C.c_int64 * 5), ("logical_sync_last", C.c_int64 * 5),
                 ("f_norm", C.c_double), ("dx_norm", C.c_double), ("r_ratio_min", C.c_double),
-                ("loo", C.c_double), ("breakdown", C.c_int32), ("pad1", C.c_int32)]
+                ("loo", C.c_double), ("breakdown", C.c_int32), ("breakdown_count", C.c_int32)]
 
 
 def _load():
@@ -182,6 +182,7 @@ class Stats:
     r_ratio_min: float
     loo: float
     breakdown: bool
+    breakdown_count: int
 
 
 def aa_stats(h: int, loo: bool = False, reset: bool = False) -> Stats:
@@ -191,7 +192,8 @@ def aa_stats(h: int, loo: bool = False, reset: bool = False) -> Stats:
         raise AAError(rc, "aa_stats")
     return Stats(s.iter, s.m_i, s.sync_points_last, s.allreduce_last, s.allreduce_total,
                  dict(zip(PHASES, list(s.logical_sync))), dict(zip(PHASES, list(s.logical_sync_last))),
-                 s.f_norm, s.dx_norm, s.r_ratio_min, s.loo, bool(s.breakdown))
+                 s.f_norm, s.dx_norm, s.r_ratio_min, s.loo, bool(s.breakdown),
+                 int(s.breakdown_count))
 
 
 def aa_reset(h: int) -> None:

@@ -62,9 +62,11 @@ struct SmallState {
   double f2;                 // ||f_i||^2 (global) of the last step
   double rratio_min;         // min R_kk / ||Delta f||
   double last_rkk;
-  int breakdown;             // sticky
+  int breakdown;             // sticky until aa_reset: a step broke down (reading A12); while set,
+                             // every step degrades to gamma = 0 (x_{i+1} = G(x_i))
   unsigned int counter;      // cross-CTA arrival ticket
   int xchg_timeout;          // sticky: a fused peer exchange timed out
+  int breakdown_count;       // steps that broke down since aa_create (kept by aa_reset)
 };
 
 // K1 reduction-slot layout (words), identical on host and device.
@@ -144,6 +146,7 @@ struct alignas(64) KParams {
   double* lmbox;
   double* red;      // reduction slots (slot s at red + s*LRED)
   double* part;     // per-CTA partials (CTA b at part + b*LRED)
+  int* bd_host;     // device alias of the handle's mapped pinned breakdown word (polled by aa_step)
 };
 
 // ------------------------------------------------------------------ PTX wrappers

@@ -51,6 +51,7 @@ struct HeadArea {
   int lcol[MMAX + 2];
   int rcol[4];
   int na, nr, is_last, gdone;   // gdone: Givens rotations published (K4, ICWY SMALL)
+  int bd;                       // K4: this step degrades to gamma = 0 (breakdown, reading A12)
 };
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -183,7 +184,17 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   for (int j = lane; j <= k; j += 32) cvec2[j] = cvec[j];
   __syncwarp();
   k3_back_subst<LDR>(Rw, cvec2, H.coef, k + 1);  // gamma -> H.coef[0..k]
-  if (p.beta_on) {
+  // breakdown (reading A12): R_kk <= eps_a ||Delta f|| (or NaN), or an
+  // earlier step of this window broke down (sticky until aa_reset): the step degrades to
+  // gamma = 0, x_{i+1} = G(x_i).  Every CTA (and every rank) takes the same decision: rkk
+  // and ||Delta f|| are global reduction results, eps_a is the same on every rank.
+  const bool bd = !(rkk > p.eps_a * sqrt(red0[1])) || p.st->breakdown != 0;
+  if (bd) {
+    __syncwarp();
+    for (int j = lane; j <= k; j += 32) H.coef[j] = 0.0;
+    if (lane == 0) H.bd = 1;
+  }
+  if (p.beta_on && !bd) {
     for (int j = lane; j <= k; j += 32) {
       double fs;
       if (j == k) fs = 1.0 / rkk;
@@ -563,7 +574,10 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   K4Head hd{};
   if (blockIdx.x == 0) AA_TL(0);
   if constexpr (OP == OP_K4 || OP == OP_K2_ICWY) {
-    if (OP == OP_K4 && tid == 0) H.gdone = 0;
+    if (OP == OP_K4 && tid == 0) {
+      H.gdone = 0;
+      H.bd = 0;
+    }
     stage_small<OP>(p, scratch);
     __syncthreads();
   }
@@ -779,14 +793,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           const double x = ldV(p, S, 1, r, rows, grow);
           double x0 = g, x1 = 0.0;
           int j = 0;
+          const bool bd = H.bd != 0;     // breakdown: x_{i+1} = G(x_i) exactly
 #pragma unroll 2
-          for (; j + 1 <= k; j += 2) {
+          for (; j + 1 <= k && !bd; j += 2) {
             x0 -= H.coef[j] * S[(size_t)j * TR + r];
             x1 -= H.coef[j + 1] * S[(size_t)(j + 1) * TR + r];
           }
-          if (j <= k) x0 -= H.coef[j] * S[(size_t)j * TR + r];
+          if (j <= k && !bd) x0 -= H.coef[j] * S[(size_t)j * TR + r];
           double xn = x0 + x1;
-          if (p.beta_on) {
+          if (p.beta_on && !bd) {
             double t = S[(size_t)(vb + 2) * TR + r];
             for (int jj = 0; jj <= k; ++jj) t -= H.coef2[jj] * S[(size_t)(k + 1 + jj) * TR + r];
             xn -= H.scal[0] * t;
@@ -954,7 +969,14 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       const double dfn = sqrt(hd.df2);
       const double ratio = dfn > 0.0 ? hd.rkk / dfn : 0.0;
       if (ratio < st->rratio_min) st->rratio_min = ratio;
-      if (!(hd.rkk > p.eps_a * dfn)) st->breakdown = 1;   // reading A12
+      if (!(hd.rkk > p.eps_a * dfn)) {   // reading A12: this step's column is dependent
+        st->breakdown = 1;
+        st->breakdown_count += 1;
+        if (p.bd_host) {   // the mapped pinned word aa_step polls (without blocking)
+          *reinterpret_cast<volatile int*>(p.bd_host) = 1;
+          __threadfence_system();
+        }
+      }
       if (!(p.flags & F_EXT_DF)) {
         st->f2 = p.red[0];
         st->dx2_local = outv[0];

@@ -75,6 +75,8 @@ struct aa_ctx {
   SmallState* st = nullptr;
   double *red = nullptr, *part = nullptr;
   double *hx = nullptr, *hg = nullptr, *hxn = nullptr;  // staging for aa_step_host
+  int* bd_host = nullptr;   // mapped pinned breakdown word (written by K4, polled by aa_step)
+  int* bd_dev = nullptr;    // its device alias
   ncclComm_t comm = nullptr;
   bool own_comm = false;
   // window bookkeeping (host; depends only on i, m_i)
@@ -357,7 +359,7 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
       occ_val[dev][occ_n[dev]++] = per_sm;
     }
   }
-  const long long ntiles = (p.n + p.tr - 1) / p.tr;
+  const long long ntiles = (p.n - p.rbeg + p.tr - 1) / p.tr;
   long long grid = std::min<long long>(ntiles, (long long)c->sms * per_sm);
   if (grid < 1) grid = 1;
   // K4 when the tiles do not fill the GPU: one extra CTA (CTA 0) writes the next factor
@@ -551,6 +553,7 @@ KParams base_params(aa_ctx* c) {
   p.rbeg = 0;
   p.chunk_first = 1;
   p.chunk_last = 1;
+  p.bd_host = c->bd_dev;
   return p;
 }
 
@@ -858,6 +861,13 @@ static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant,
   c->stream = (cudaStream_t)cuda_stream;
   c->own_stream = false;
   const size_t vbytes = (size_t)c->ld * sizeof(double);
+  if (cudaHostAlloc(&c->bd_host, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->bd_dev), c->bd_host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    c->bd_host = nullptr;
+    return bail(AA_ERR_NOMEM);
+  }
+  *reinterpret_cast<volatile int*>(c->bd_host) = 0;
   if (cudaMalloc(&c->Q, vbytes * m) != cudaSuccess || cudaMalloc(&c->DG, vbytes * m) != cudaSuccess ||
       cudaMalloc(&c->fp, vbytes) != cudaSuccess || cudaMalloc(&c->gp, vbytes) != cudaSuccess ||
       cudaMalloc(&c->st, sizeof(SmallState)) != cudaSuccess ||
@@ -894,6 +904,19 @@ static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant,
       return bail(AA_ERR_NCCL);
     }
     c->own_comm = true;
+  }
+  if (nranks > 1) {
+    // n_global = sum of the ranks' n_local (collective, once): the default breakdown threshold
+    // eps_a = 10 eps sqrt(n_global) must be the same on every rank (reading A12), including
+    // uneven shards
+    double* tmp = c->red + (size_t)(NSLOT - 1) * LRED;
+    double nl = (double)n_local, ng = 0.0;
+    if (cudaMemcpy(tmp, &nl, sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) return bail(AA_ERR_CUDA);
+    if (nccl().AllReduce(tmp, tmp, 1, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return bail(AA_ERR_NCCL);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess ||
+        cudaMemcpy(&ng, tmp, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return bail(AA_ERR_CUDA);
+    c->n_global = (int64_t)ng;
   }
   *out = c;
   return AA_OK;
@@ -1017,6 +1040,7 @@ static void init_small(SmallState* hs, bool keep_scalars, const SmallState* old)
   if (keep_scalars && old) {
     hs->dx2_local = old->dx2_local;
     hs->f2 = old->f2;
+    hs->breakdown_count = old->breakdown_count;
   }
 }
 
@@ -1035,6 +1059,7 @@ int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out) 
   RET_IF(check_handle(h));
   if (!x0 || !gx0 || !x1_out) return AA_ERR_ARG;
   RET_IF(reset_small(h));
+  *reinterpret_cast<volatile int*>(h->bd_host) = 0;
   if (h->eps_a < 0.0) h->eps_a = 10.0 * DBL_EPSILON * sqrt((double)h->n_global);
   const int grid = h->sms * 4;
   aa_init_kernel<<<grid, 256, 0, h->stream>>>(x0, gx0, x1_out, h->fp, h->gp, h->n);
@@ -1050,6 +1075,12 @@ int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out) 
 int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next) {
   RET_IF(check_handle(h));
   if (!h->inited) return AA_ERR_STATE;
+  // a breakdown seen by an earlier step (mapped pinned word, polled without blocking):
+  // refuse until aa_reset.  One rank only: ranks could see the word at different times and
+  // must not diverge in their collective call sequences; with nranks > 1 the breakdown is
+  // surfaced by aa_stats (collective, after a synchronisation), and steps enqueued before
+  // that degrade to gamma = 0 on every rank alike.
+  if (h->nranks == 1 && *reinterpret_cast<volatile int*>(h->bd_host)) return AA_ERR_BREAKDOWN;
   if (!x_i || !gx_i || !x_next || !aligned16(x_i) || !aligned16(gx_i) || !aligned16(x_next))
     return AA_ERR_ARG;
   int rc;
@@ -1066,10 +1097,15 @@ int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x
   if (!h->inited) return AA_ERR_STATE;
   if (!x_i || !gx_i || !x_next) return AA_ERR_ARG;
   const size_t vb = (size_t)h->n * sizeof(double);
-  if (!h->hx) {
-    if (cudaMalloc(&h->hx, vb) != cudaSuccess || cudaMalloc(&h->hg, vb) != cudaSuccess ||
-        cudaMalloc(&h->hxn, vb) != cudaSuccess) {
+  if (!h->hx || !h->hg || !h->hxn) {
+    if ((!h->hx && cudaMalloc(&h->hx, vb) != cudaSuccess) || (!h->hg && cudaMalloc(&h->hg, vb) != cudaSuccess) ||
+        (!h->hxn && cudaMalloc(&h->hxn, vb) != cudaSuccess)) {
       cudaGetLastError();
+      // all or nothing: a later call retries the allocation (not sticky)
+      cudaFree(h->hx);
+      cudaFree(h->hg);
+      cudaFree(h->hxn);
+      h->hx = h->hg = h->hxn = nullptr;
       return AA_ERR_NOMEM;
     }
   }
@@ -1177,46 +1213,67 @@ int aa_stats(aa_handle_t h, struct aa_stats* out, int flags) {
     out->logical_sync[i] = h->logical[i];
     out->logical_sync_last[i] = h->logical_last[i];
   }
-  if (h->failed != AA_OK) return h->failed;
-  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   struct {
-    double dx2, f2, rmin;
-    int bd;
+    double dx2 = 0.0, f2 = 0.0, rmin = 0.0;
+    int bd = 0, bdc = 0;
   } hs;
-  {
+  int status = h->failed;
+  if (status == AA_OK) {
     // only the scalar tail of SmallState (the factors stay on the device)
     constexpr size_t off = offsetof(SmallState, dx2_local);
     unsigned char tail[sizeof(SmallState) - off];
-    cudaError_t e = cudaMemcpy(tail, reinterpret_cast<unsigned char*>(h->st) + off, sizeof(tail),
-                               cudaMemcpyDeviceToHost);
-    CUDA_TRY(h, e);
-    auto fld = [&](size_t o) { return tail + (o - off); };
-    double dx2l, dx2g;
-    int xto;
-    memcpy(&dx2l, fld(offsetof(SmallState, dx2_local)), sizeof(double));
-    memcpy(&dx2g, fld(offsetof(SmallState, dx2_global)), sizeof(double));
-    memcpy(&hs.f2, fld(offsetof(SmallState, f2)), sizeof(double));
-    memcpy(&hs.rmin, fld(offsetof(SmallState, rratio_min)), sizeof(double));
-    memcpy(&hs.bd, fld(offsetof(SmallState, breakdown)), sizeof(int));
-    memcpy(&xto, fld(offsetof(SmallState, xchg_timeout)), sizeof(int));
-    hs.dx2 = (h->conv_norm == 1 && h->nranks > 1) ? dx2g : dx2l;
-    if (xto) {
-      fprintf(stderr, "libaa: fused peer exchange timed out\n");
-      return fail(h, AA_ERR_NCCL);
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(tail, reinterpret_cast<unsigned char*>(h->st) + off, sizeof(tail), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "libaa: CUDA error %s in aa_stats\n", cudaGetErrorString(e));
+      status = fail(h, AA_ERR_CUDA);
+    } else {
+      auto fld = [&](size_t o) { return tail + (o - off); };
+      double dx2l, dx2g;
+      int xto;
+      memcpy(&dx2l, fld(offsetof(SmallState, dx2_local)), sizeof(double));
+      memcpy(&dx2g, fld(offsetof(SmallState, dx2_global)), sizeof(double));
+      memcpy(&hs.f2, fld(offsetof(SmallState, f2)), sizeof(double));
+      memcpy(&hs.rmin, fld(offsetof(SmallState, rratio_min)), sizeof(double));
+      memcpy(&hs.bd, fld(offsetof(SmallState, breakdown)), sizeof(int));
+      memcpy(&hs.bdc, fld(offsetof(SmallState, breakdown_count)), sizeof(int));
+      memcpy(&xto, fld(offsetof(SmallState, xchg_timeout)), sizeof(int));
+      hs.dx2 = (h->conv_norm == 1 && h->nranks > 1) ? dx2g : dx2l;
+      if (xto) {
+        fprintf(stderr, "libaa: fused peer exchange timed out\n");
+        status = fail(h, AA_ERR_NCCL);
+      }
     }
   }
-  if (h->nranks > 1 && h->conv_norm == 0) {
+  // collective (nranks > 1): every rank contributes {lagged ||dx||^2 partial, error flag} to ONE
+  // allreduce, so the ranks agree on the outcome and none is left waiting in a collective its
+  // peers skipped; a rank whose communicator itself failed cannot take part
+  bool peer_failed = false;
+  if (h->nranks > 1 && h->comm && nccl().ok && !(h->failed == AA_ERR_NCCL && !h->fused)) {
     double* tmp = h->red + (size_t)(NSLOT - 1) * LRED;
-    CUDA_TRY(h, cudaMemcpyAsync(tmp, &hs.dx2, sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    ncclResult_t r = nccl().AllReduce(tmp, tmp, 1, kNcclFloat64, kNcclSum, h->comm, h->stream);
-    if (r != 0) return fail(h, AA_ERR_NCCL);
-    CUDA_TRY(h, cudaMemcpyAsync(&hs.dx2, tmp, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    double v[2] = {(h->conv_norm == 0 && status == AA_OK) ? hs.dx2 : 0.0, status != AA_OK ? 1.0 : 0.0};
+    cudaError_t e = cudaMemcpyAsync(tmp, v, sizeof(v), cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess && nccl().AllReduce(tmp, tmp, 2, kNcclFloat64, kNcclSum, h->comm, h->stream) != 0) {
+      status = fail(h, AA_ERR_NCCL);
+      return status;
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(v, tmp, sizeof(v), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return fail(h, AA_ERR_CUDA);
+    if (h->conv_norm == 0) hs.dx2 = v[0];
+    peer_failed = v[1] > 0.0;
+  }
+  if (status != AA_OK) return status;
+  if (peer_failed) {
+    fprintf(stderr, "libaa: a peer rank's handle failed\n");
+    return fail(h, AA_ERR_NCCL);
   }
   out->f_norm = sqrt(hs.f2);
   out->dx_norm = (h->conv_norm == 2) ? -1.0 : sqrt(hs.dx2);
   out->r_ratio_min = hs.rmin;
   out->breakdown = hs.bd;
+  out->breakdown_count = hs.bdc;
   if ((flags & AA_STATS_LOO) && h->mi >= 1) {
     KParams p = base_params(h);
     p.op = OP_GRAM;
@@ -1269,6 +1326,7 @@ int aa_reset(aa_handle_t h) {
   delete old;
   delete hs;
   if (e != cudaSuccess) return fail(h, AA_ERR_CUDA);
+  *reinterpret_cast<volatile int*>(h->bd_host) = 0;
   h->ver = 0;
   return AA_OK;
 }
@@ -1302,6 +1360,7 @@ int aa_destroy(aa_handle_t h) {
   cudaFree(h->hx);
   cudaFree(h->hg);
   cudaFree(h->hxn);
+  if (h->bd_host) cudaFreeHost(h->bd_host);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return AA_OK;
@@ -1377,13 +1436,6 @@ int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384) {
   if (!enable && h->tl) {
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     cudaFree(h->tl);
-  if (h->cstream) {
-    cudaStreamDestroy(h->cstream);
-    for (int i = 0; i < 8; ++i) {
-      cudaEventDestroy(h->chunk_evH[i]);
-      cudaEventDestroy(h->chunk_evK[i]);
-    }
-  }
     h->tl = nullptr;
   }
   if (out384 && h->tl) {
@@ -1398,8 +1450,9 @@ int aa_fill_uniform(double* out, int64_t n, int64_t offset, uint64_t seed, uint6
   if (!out || n < 0) return AA_ERR_ARG;
   if (n == 0) return AA_OK;
   const unsigned long long base = seed + stream * (1ull << 48) + (unsigned long long)offset;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return AA_ERR_CUDA;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   aa_fill_uniform_kernel<<<sms * 8, 256, 0, (cudaStream_t)cuda_stream>>>(out, n, base, lo, hi - lo);
   if (cudaGetLastError() != cudaSuccess) return AA_ERR_CUDA;
   return AA_OK;

@@ -1,12 +1,17 @@
-"""Parity at the bench's full size (config 2: n_local = 1e8 fp64, m = 20 and 50), in the
-launch configuration bench.py times.
+"""Parity at the bench's full size (config 2: n_local = 1e8 fp64) in the launch configuration
+bench.py times, for every window depth the bench and its --sweep publish (m = 5, 10, 20,
+50) and every variant (MGS, ICWY, ICWY SMALL, CGS-2, DCGS-2).
 
-The problem is block-constant: d and b are constant on 1000 equal row blocks of 1e5
-rows, so every AA iterate is block-constant and — the inner product being 1e5 times the
-1000-row one, which leaves gamma unchanged — equal blockwise to the iterate of the
-1000-row problem, which the oracle runs (pinned on CPU by
-tests/test_oracle_pins.py::test_block_constant_reduction_property).  Checked per
-iteration on one sampled row per block; rows within a block must be bitwise equal.
+The problem is PERIODIC: d and b repeat with period P = 3125 rows (d_i = d_small[i mod P]).
+P divides 1e8 (1e8 = 32000 P) but no tile height (powers of two up to 1024, and 252 / 124 /
+60 / 28 for the Gram tiles), so every tile holds distinct rows of several periods.  Every
+AA iterate is then periodic -- each row's arithmetic depends only on its own d, b, x and on
+the replicated small factors -- so all 32000 periods must be bitwise equal (an intra-tile
+row mix-up breaks that), and one period equals the iterate of the P-row problem the oracle
+runs: the window columns are the P-row ones repeated, their inner products are 32000 times
+the P-row ones, which scales R and Q^T f alike and leaves gamma unchanged (the LS problem is
+the same up to a constant factor).  Checked per iteration against O2 at 1e-10 (SURVEY.md
+§8(c) criterion 1) until the residual reaches rounding level.
 """
 import numpy as np
 import pytest
@@ -18,49 +23,61 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from aa_inputs import problems  # noqa: E402
-from oracle import EPS, aa_variant, VARIANTS  # noqa: E402
+from oracle import EPS, aa_variant  # noqa: E402
 from paper_2110_09667_b200 import aa  # noqa: E402
 
-N, P = 100_000_000, 1000
+N, P = 100_000_000, 3125
 W = N // P
+assert W * P == N and all(P % t for t in (1024, 512, 256, 128, 64, 32, 252, 124, 60, 28))
+
+CASES = [(v, o, m) for m in (5, 10, 20, 50)
+         for v, o in (("mgs", None), ("icwy", None), ("icwy", "small"), ("cgs2", None), ("dcgs2", None))]
 
 
 @pytest.fixture(scope="module")
-def big_problem():
-    w, d, b = problems.block_constant(N, P)
-    assert (w == W).all()
-    dt = torch.tensor(d, device="cuda").repeat_interleave(W)
-    bt = torch.tensor(b, device="cuda").repeat_interleave(W)
+def periodic():
+    d, b = problems.diagonal(P)
+    dt = torch.tensor(d, device="cuda").repeat(W)
+    bt = torch.tensor(b, device="cuda").repeat(W)
     return d, b, dt, bt
 
 
-@pytest.mark.parametrize("variant,m,iters", [(v, 20, 26) for v in VARIANTS] + [("dcgs2", 50, 56), ("icwy", 50, 56)])
-def test_full_size_block_constant(big_problem, variant, m, iters):
-    d, b, dt, bt = big_problem
-    ref = aa_variant(lambda x: d * x + b, np.zeros(P), m, variant, iters)
-    stream = torch.cuda.current_stream()
-    s = aa.AndersonSolver(N, m, variant, stream=stream)
+@pytest.mark.parametrize("variant,icwy_delete,m", CASES,
+                         ids=[f"{v}{'_small' if o else ''}-m{m}" for v, o, m in CASES])
+def test_full_size_periodic(periodic, variant, icwy_delete, m):
+    d, b, dt, bt = periodic
+    iters = m + 6                                   # start-up and 6 recycle iterations
+    ref = aa_variant(lambda x: d * x + b, np.zeros(P), m, variant, iters,
+                     icwy_delete=icwy_delete or "rebuild")
+    s = aa.AndersonSolver(N, m, variant, stream=torch.cuda.current_stream(), icwy_delete=icwy_delete)
     x = torch.zeros(N, dtype=torch.float64, device="cuda")
     xn = torch.empty_like(x)
     s.init(x, torch.addcmul(bt, dt, x), xn)
     x, xn = xn, x
-    starts = torch.arange(0, N, W, device="cuda")
-    worst = 0.0
+    # rounding level: past it the window columns are noise and only finiteness is meaningful
     K = next((i for i, f in enumerate(ref.f_norms) if f < 1e-11 * np.linalg.norm(ref.x1)), iters)
+    worst, worst_f = 0.0, 0.0
     for i in range(iters):
         s.step(x, torch.addcmul(bt, dt, x), xn)
         x, xn = xn, x
+        st = s.stats()
+        assert not st.breakdown
+        xv = x.view(W, P)
+        assert torch.equal(xv, xv[:1].expand(W, P)), f"iterate {i + 2}: periods differ"
         if i < K:
-            samp = x[starts].cpu().numpy()
-            last = x[starts + W - 1].cpu().numpy()
-            assert np.array_equal(samp, last), "rows of a block must be bitwise equal"
-            r = ref.xs[i]
-            worst = max(worst, float(np.linalg.norm(samp - r) / np.linalg.norm(r)))
+            a, r = x[:P].cpu().numpy(), ref.xs[i]
+            worst = max(worst, float(np.linalg.norm(a - r) / np.linalg.norm(r)))
+            fo = ref.f_norms[i]
+            xo = np.linalg.norm(ref.xs[i - 1] if i else ref.x1)
+            worst_f = max(worst_f, abs(st.f_norm / np.sqrt(W) - fo) / (1e-10 * fo + 100 * EPS * xo))
+        else:
+            assert torch.isfinite(x[:P]).all()
     st = s.stats(loo=True)
     s.close()
     assert worst <= 1e-10, worst
+    assert worst_f <= 1.0, worst_f
     assert st.m_i == m
     # LOO of a length-1e8 factorisation carries the summation error of its own inner
     # products (each of the 148x32 lanes accumulates ~2e4 products): floor
-    # 10 m eps sqrt(n / 4736); the 1000-row oracle cannot see that term.
+    # 10 m eps sqrt(n / 4736); the P-row oracle cannot see that term.
     assert st.loo <= max(10 * ref.loo[-1], 10 * m * EPS * np.sqrt(N / 4736)), (st.loo, ref.loo[-1])

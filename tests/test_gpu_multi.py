@@ -16,10 +16,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("mode", ["torch_comm", "torch_comm_fused"])
+@pytest.mark.parametrize("mode", ["torch_comm", "torch_comm_fused", "unique_id", "unique_id_fused"])
 def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
-    """NCCL allreduce per reduction (torch_comm) or the fused one-shot NVLink exchange in
-    the producing kernel's last CTA (torch_comm_fused)."""
+    """NCCL allreduce per reduction (torch_comm*: torch's communicator borrowed through
+    aa_create_with_comm; unique_id*: libaa's own communicator from aa_comm_unique_id +
+    aa_create, the north-star rendezvous) or the fused one-shot NVLink exchange in the
+    producing kernel's last CTA (*_fused).  Also SURVEY.md §8(c) criterion 6 (the p-rank
+    iterates vs the same run on one GPU, <= 1e-13) and the breakdown decisions (reading
+    A12) identical on every rank and equal to the oracle's restart policy."""
     from aa_inputs import problems
     from oracle import aa_variant
     world = min(torch.cuda.device_count(), 4)
@@ -58,6 +62,15 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
             assert ars[i - 1] == want, (variant, i, ars)
         assert r["gamma_identical_across_ranks"]
         assert r["loo"] < 1e-12
+        assert r["x_vs_p1"] <= 1e-13, (variant, r["x_vs_p1"])
+    assert rep["breakdown_flags_identical_across_ranks"]
+    d5, b5 = problems.diagonal(n, 0.5, 0.99)
+    for variant, r in rep["breakdown"].items():
+        o2 = aa_variant(lambda x: d5 * x + b5, np.zeros(n), 2, variant, 10, breakdown="restart",
+                        breakdown_eps=0.5, record_loo=False)
+        assert r["flags"] == o2.breakdown and any(r["flags"])
+        for a, ref in zip(r["xs"], o2.xs):
+            assert np.linalg.norm(np.array(a) - ref) <= 1e-10 * np.linalg.norm(ref), variant
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")

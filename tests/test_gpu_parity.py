@@ -101,14 +101,19 @@ def test_ragged_sizes_and_windows(n, m, variant):
     d, b = problems.diagonal(n)
     dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
     iters = min(2 * m + 6, 30)
-    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters)
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters, breakdown="restart")
     gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, iters)
-    # stop comparing once the oracle has converged to rounding level
+    # stop comparing once the oracle has converged to rounding level (there, at n = 1, the
+    # next Delta f can be exactly 0 on one side and not on the other: breakdown decisions at
+    # rounding level are not comparable)
     K = next((i for i, f in enumerate(o2.f_norms) if f < 1e-11 * np.linalg.norm(o2.x1)), iters)
     if K > 0:
         assert _rel_x(gpu, o2, K) <= 1e-10
     for i in range(K):
         assert gpu.ledgers[i] == {k_: v_ for k_, v_ in o2.ledgers[i].items()}
+        assert gpu.breakdown[i] == o2.breakdown[i]
+    for a in gpu.xs:
+        assert np.isfinite(a).all()
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -335,15 +340,18 @@ def test_no_writes_outside_caller_buffers(n):
             g.copy_(dt * x + bt)
             s.step(x, g, xn)
             x, xn = xn, x
+            assert torch.isfinite(x).all()
+            if s.stats().breakdown:      # n <= 5: later Delta f are dependent; restart
+                s.reset()
         s.stats(loo=True)
-        s.delete_oldest()
+        if s.stats().m_i >= 1:
+            s.delete_oldest()
         g.copy_(dt * x + bt)
         s.step(x, g, xn)
         torch.cuda.synchronize()
         for t in bufs:
             assert torch.isnan(t[:pad]).all() and torch.isnan(t[pad + n:]).all(), v
-        if not s.stats().breakdown:      # n = 1: every later Delta f is dependent (R_kk = 0)
-            assert torch.isfinite(xn).all()
+        assert torch.isfinite(xn).all()   # a breakdown degrades the step to x_next = G(x_i)
         s.close()
 
 
@@ -403,3 +411,42 @@ def test_output_may_alias_inputs(variant):
         assert np.all(np.isfinite(ref))
         for mode in ("in_place", "into_g"):
             assert np.array_equal(runs[(mode, beta)], ref), (mode, beta)
+
+
+@pytest.mark.parametrize("icwy_delete", ["separate", "merged", "small"])
+def test_icwy_T_is_the_gram_of_q_when_q_is_far_from_orthogonal(icwy_delete):
+    """ICWY's T = I + strict_lower(Q^T Q) (reading A5) and its update after
+    QRDelete (P:319-325 rebuild, A6; merged; A6b SMALL) checked where it matters: on the
+    Pr6/Pr7 window (d in U[0.9, 0.99], m = 20) Q loses orthogonality (LOO 1e-8 .. 1 during
+    start-up, ~1e-6 after recycling starts), so T's off-diagonals are far from 0 (T = I
+    fails).  After every step the GPU's T rows 0..k-1 must equal the strict lower Gram of the
+    GPU's own normalised columns 0..k-1 (aa_get_q; k = m_i - 1, the newest column's row is
+    formed by the next step) to 1e-12 absolute."""
+    n, m, iters = 20011, 20, 30
+    d, b = problems.diagonal(n, 0.9, 0.99)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    s = aa.AndersonSolver(n, m, "icwy", stream=torch.cuda.current_stream(), icwy_delete=icwy_delete,
+                          breakdown_eps=0.0)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    xn = torch.empty_like(x)
+    s.init(x, dt * x + bt, xn)
+    x, xn = xn, x
+    biggest, worst = 0.0, 0.0
+    for i in range(iters):
+        s.step(x, dt * x + bt, xn)
+        x, xn = xn, x
+        mi = s.stats().m_i
+        k = mi - 1
+        if k < 2:
+            continue
+        q = torch.empty(n * mi, dtype=torch.float64, device="cuda")
+        aa.aa_get_q(s.h, q)
+        Q = q.cpu().numpy().reshape(mi, n).T[:, :k]
+        _, T, _, _ = aa.aa_get_small(s.h, m, mi)
+        G = np.tril(Q.T @ Q, -1)
+        worst = max(worst, float(np.max(np.abs(np.tril(T[:k, :k], -1) - G))))
+        biggest = max(biggest, float(np.max(np.abs(G))))
+        assert np.all(np.diag(T[:k, :k]) == 1.0)
+    s.close()
+    assert biggest > 1e-2, biggest            # non-vacuous: T = I would be off by this much
+    assert worst <= 1e-12, (worst, biggest)
