@@ -197,8 +197,12 @@ def run_reference(args):
     n_sample = int(args.ref_n)
     us, cores, raw = oracle_sample(args.m, args.variant, n_sample, args.steps, args.warmup, n_target)
     line = {
+        # value: the oracle's time per recycle iteration scaled to the workload's n_local (it is
+        # bandwidth-bound: linear in n); ms_per_step: what one timed step of the sample really
+        # took on this host, so steps x ms_per_step is the run's actual timed region
         "impl": "reference", "metric": METRIC, "value": us, "unit": "us/iter", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": raw / 1e3,
+        "ms_per_step_scaled_to_n_local": us / 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(args),
         "cpu_baseline": {"value": us, "unit": "us/iter", "cores": cores, "kind": "oracle",
@@ -218,6 +222,7 @@ def _config(args):
                          "G(x)=d*x+b, d~U[-0.9,0.9), b~U[-1,1) (SplitMix64 seed 9667), x0=0"),
             "n_local": int(args.n_local), "m": args.m, "variant": args.variant,
             "parallelism": f"rows{args.gpus}", "l2": "inputs larger than L2 (0.8 GB per vector)",
+            "breakdown_eps": 0.0,
             "timed": "aa_step only (CUDA events on the handle's stream); G excluded"}
 
 
@@ -233,8 +238,13 @@ def main():
                     help="strong scaling (config 3: 4e8): n_local = n_global / N instead of --n-local")
     ap.add_argument("--variant", default="dcgs2", choices=VARIANTS)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--ref-n", type=float, default=1e6)
-    ap.add_argument("--sweep", action="store_true", help="also sweep m in {5,10,20,50} x variants")
+    ap.add_argument("--ref-n", type=float, default=1e7,
+                    help="--impl reference: rows of the oracle's sample (scaled linearly to n_local)")
+    ap.add_argument("--cpu-n", type=float, default=2e6,
+                    help="cpu_baseline leg of the GPU arm: rows of the oracle's bounded sample")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the default m sweep (m in {5,10,20,50} x variants, 3 recycle steps each)")
+    ap.add_argument("--sweep", action="store_true", help=argparse.SUPPRESS)   # the sweep is the default
     ap.add_argument("--sweep-n", action="store_true",
                     help="latency regime: n_local in {1e3..1e7} x variants at --m (paper's GPU size 1.5e6, P:513)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -317,8 +327,13 @@ def main():
     ar_mode = {"mode": "ncclAllReduce" if world > 1 else "none (1 rank)"}
 
     def make_solver(nl, m, variant, **kw):
+        # the kernel study times full recycle steps: with m = 50 (and m = 20 after the timed
+        # steps) this problem's residual is at rounding level, where a new column can pass the
+        # breakdown threshold (reading A12) and the step would degrade to x = G(x) (skipping
+        # K4's products) -- the breakdown test is set to R_kk = 0 / NaN only (eps_a = 0)
+        kw.setdefault("breakdown_eps", 0.0)
         s = aa.AndersonSolver(nl, m, variant, rank=rank, nranks=world, unique_id=uid, nccl_comm=comm,
-                              stream=stream, n_global=nl * world, **kw)
+                              stream=stream, **kw)
         if args.fused_ar and world > 1:
             try:
                 aa.aa_set_option(s.h, aa.OPT_FUSED_ALLREDUCE, 1)
@@ -366,6 +381,19 @@ def main():
         step_ms = [a.elapsed_time(b_) for a, b_ in ev]
         ms_t, cnt = aa.aa_timings(s.h, reset=True)
         st = s.stats()
+        # start-up: the m window-filling iterations i = 1..m, timed again after
+        # aa_reset on the warm handle (CUDA events around the whole sequence)
+        s.reset()
+        e_su = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        barrier()
+        e_su[0].record(stream)
+        for i in range(m):
+            s.step(x, Gi(x, i), xn)
+            x, xn = xn, x
+        e_su[1].record(stream)
+        barrier()
+        startup_ms = e_su[0].elapsed_time(e_su[1])
+        aa.aa_timings(s.h, reset=True)
         res = {"ms_per_step": max_over_ranks(float(np.mean(step_ms))),
                "ms_min": max_over_ranks(float(np.min(step_ms))),
                "k1_ms": max_over_ranks(ms_t[0] / max(cnt[0], 1)),
@@ -374,7 +402,8 @@ def main():
                "allreduce_ms_per_step": max_over_ranks(ms_t[3] / steps),
                "launches_per_step": launches / steps, "launches": launches,
                "sync_points_per_step": st.sync_points_last, "allreduce_per_step": st.allreduce_last,
-               "f_norm": st.f_norm, "step_ms": [round(v, 4) for v in step_ms]}
+               "f_norm": st.f_norm, "step_ms": [round(v, 4) for v in step_ms],
+               "startup_ms_total": max_over_ranks(startup_ms), "startup_iters": m}
         e2e_res = None
         if e2e:
             nh = 3
@@ -460,21 +489,41 @@ def main():
                            "launches": r["launches_per_step"], "k1_ms": r["k1_ms"],
                            "k2_ms_per_step": r["k2_ms_per_step"], "k4_ms": r["k4_ms"],
                            "allreduce_ms_per_step": r["allreduce_ms_per_step"], "ms_min": r["ms_min"],
-                           "step_ms_rank0": r["step_ms"]}
+                           "startup_ms_total": r["startup_ms_total"], "step_ms_rank0": r["step_ms"]}
     sweep = {}
-    if args.sweep:
+    if not args.no_sweep and not args.only_headline:
+        # north_star's range m in {5..50}: every variant, 3 recycle steps each
         for m in (5, 10, 20, 50):
             for v in VARIANTS + EXTRA_VARIANTS:
+                if m == args.m and v in variants:
+                    e = variants[v]
+                    sweep[f"{v}_m{m}"] = {k_: e[k_] for k_ in ("us_per_iter", "step_hbm_frac", "k1_frac",
+                                                               "startup_ms_total")}
+                    sweep[f"{v}_m{m}"]["step_frac_8tbs"] = step_bytes(v, m, V) / (e["us_per_iter"] * 1e-6) / 8e12
+                    continue
                 r, _, _ = measure(v, m, 3, 3)
                 sweep[f"{v}_m{m}"] = {"us_per_iter": r["ms_per_step"] * 1e3,
                                       "step_hbm_frac": step_bytes(v, m, V) / (r["ms_per_step"] * 1e-3) / (peak * 1e9),
-                                      "k1_frac": k1_bytes(m, V) / (r["k1_ms"] * 1e-3) / (peak * 1e9)}
+                                      "step_frac_8tbs": step_bytes(v, m, V) / (r["ms_per_step"] * 1e-3) / 8e12,
+                                      "k1_frac": k1_bytes(m, V) / (r["k1_ms"] * 1e-3) / (peak * 1e9),
+                                      "startup_ms_total": r["startup_ms_total"]}
 
     small_n = {}
     if args.sweep_n:
         for nl in (1000, 10000, 100000, 1500000, 10000000):
             for v in VARIANTS + EXTRA_VARIANTS:
                 small_n[f"{v}_n{nl}"] = measure_n(v, args.m, nl, 20, 5)
+
+    xlat = {}
+    if world > 1 and not args.only_headline:
+        # per-exchange latency of one global reduction, 8 B .. 16 KB:
+        # the fused one-shot NVLink exchange timed inside one kernel (%globaltimer) and
+        # ncclAllReduce timed with CUDA events, 200 back to back each
+        sx = make_solver(1000, 4, "dcgs2")
+        for w in (1, 4, 16, 64, 256, 1024, 2048):
+            uf, un = aa.aa_test_exchange(sx.h, w, 200)
+            xlat[f"{8 * w}B"] = {"fused_us": max_over_ranks(uf), "nccl_us": max_over_ranks(un)}
+        sx.close()
 
     k1b = k1_bytes(args.m, V)
     achieved = k1b / (head["k1_ms"] * 1e-3) / 1e9
@@ -488,14 +537,17 @@ def main():
             "frac_of_rw_mix_ceiling": achieved / 6660.0 if args.m == 20 else None,
             "step_bytes": step_bytes(args.variant, args.m, V),
             "step_frac": step_bytes(args.variant, args.m, V) / (head["ms_per_step"] * 1e-3) / (peak * 1e9),
+            # north_star's own roofline: the step's algorithmic bytes at 8 TB/s
+            "step_frac_8tbs": step_bytes(args.variant, args.m, V) / (head["ms_per_step"] * 1e-3) / 8e12,
             "k1_share_of_step": head["k1_ms"] / head["ms_per_step"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        us, cores, raw = oracle_sample(args.m, args.variant, int(args.ref_n), 3, 1, n_local)
+        us, cores, raw = oracle_sample(args.m, args.variant, int(args.cpu_n), 3, 1, n_local)
         cpu = {"value": us, "unit": "us/iter", "cores": cores, "kind": "oracle",
-               "sample": f"O2 numpy fp64 {args.variant} m={args.m}: 3 recycle iterations at n={int(args.ref_n)} "
-                         f"({raw:.0f} us/iter) scaled x{n_local / args.ref_n:g} to n_local={n_local}"}
+               "sample": f"O2 numpy fp64 {args.variant} m={args.m}: 3 recycle iterations at n={int(args.cpu_n)} "
+                         f"({raw:.0f} us/iter) scaled x{n_local / args.cpu_n:g} to n_local={n_local}; "
+                         "1-thread and n = 1e7 / 1e8 runs: profiles/r02/oracle_baseline.json"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": head["ms_per_step"] * 1e3, "unit": "us/iter", "n_gpus": world,
@@ -508,6 +560,8 @@ def main():
                 "variants": variants}
         if sweep:
             line["sweep"] = sweep
+        if xlat:
+            line["exchange_latency"] = xlat
         if small_n:
             line["small_n"] = small_n
         print(json.dumps(line), flush=True)

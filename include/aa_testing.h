@@ -50,6 +50,14 @@ int aa_fill_uniform(double* out_dev, int64_t n, int64_t offset, uint64_t seed, u
  * use it to order phases, and ncu launch lists / PC sampling for durations. */
 int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384);
 
+/* Per-exchange latency of one global reduction, collective:
+ * `iters` back-to-back exchanges of `words` fp64 words (1 <= words <= 2304).  us_fused: the
+ * one-shot NVLink exchange (AA_OPT_FUSED_ALLREDUCE must be on; else -1), timed inside one
+ * kernel with %globaltimer; us_nccl: ncclAllReduce on the handle's communicator, timed with
+ * CUDA events on the handle's stream (one untimed call first).  Either pointer may be NULL.
+ * nranks == 1: both -1. */
+int aa_test_exchange(aa_handle_t h, int words, int iters, double* us_fused, double* us_nccl);
+
 /* Build-time facts: sm target, tile rows, stages, block size (for the report). */
 int aa_build_info(char* buf, int len);
 

@@ -27,7 +27,7 @@ PHASES = ("qradd", "qrdelete", "lsp_rhs", "norm_check", "other")
 EXPORTS = ("aa_comm_unique_id", "aa_create", "aa_create_with_comm", "aa_set_option", "aa_init", "aa_step", "aa_step_host",
            "aa_delete_oldest", "aa_stats", "aa_reset", "aa_destroy", "aa_status_string",
            "aa_test_qradd", "aa_get_small", "aa_get_q", "aa_timings", "aa_kernel_launches",
-           "aa_fill_uniform", "aa_build_info", "aa_test_timeline")
+           "aa_fill_uniform", "aa_build_info", "aa_test_timeline", "aa_test_exchange")
 
 
 class AAStatsC(C.Structure):
@@ -64,6 +64,7 @@ def _load():
         "aa_fill_uniform": (i32, [vp, i64, i64, C.c_uint64, C.c_uint64, dbl, dbl, vp]),
         "aa_build_info": (i32, [C.c_char_p, i32]),
         "aa_test_timeline": (i32, [vp, i32, vp]),
+        "aa_test_exchange": (i32, [vp, i32, i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -252,6 +253,13 @@ def aa_test_timeline_raw(h: int):
     out = np.zeros(384, dtype=np.uint64)
     _chk(_lib.aa_test_timeline(h, 1, out.ctypes.data), "aa_test_timeline")
     return out
+
+
+def aa_test_exchange(h: int, words: int, iters: int = 200):
+    """(us per fused exchange, us per ncclAllReduce) of `words` fp64 words; -1 = not available."""
+    uf, un = C.c_double(-1.0), C.c_double(-1.0)
+    _chk(_lib.aa_test_exchange(h, words, iters, C.byref(uf), C.byref(un)), "aa_test_exchange")
+    return uf.value, un.value
 
 
 def aa_build_info() -> str:

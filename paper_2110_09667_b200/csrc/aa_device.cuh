@@ -125,6 +125,8 @@ struct alignas(64) KParams {
   int nin, tr, stages;
   int vb;           // first vector column (= sum of block columns)
   int tm3d;         // column blocks use 3-D maps (TR a multiple of 256)
+  int k1_tmastore;  // K1: full tiles write their outputs with TMA stores from the stage
+                    // (rotated Q block + Delta f in one tensor store; f, G(x), Delta g 1-D)
   int beta_on;
   long long n;      // local rows
   double beta, eps_a;
@@ -138,10 +140,12 @@ struct alignas(64) KParams {
   int ver;          // factor version read by this step (written: ver ^ 1, by K4)
   // fused one-shot allreduce over NVLink peer memory (AA_OPT_FUSED_ALLREDUCE): the last
   // CTA exchanges words [xoff[e], xoff[e]+xcnt[e]) of its reduction slot, e < nxchg,
-  // with sequence numbers seq0 + e
+  // with sequence numbers xseq + 1 + e (the counter is advanced by that CTA)
   int nxchg, nranks, rank;
   int xoff[2], xcnt[2];
-  unsigned long long seq0;
+  unsigned long long* xseq;               // this rank's exchange sequence counter (device word in
+                                          // the mailbox buffer's header; never reset, so tags stay
+                                          // fresh across graph replays and aa_reset)
   double* pmbox[MAX_RANKS];               // peer q's mailbox (q == rank: local)
   double* lmbox;
   double* red;      // reduction slots (slot s at red + s*LRED)
@@ -205,6 +209,33 @@ __device__ __forceinline__ void tma_3d_g2s(void* dst, const CUtensorMap* map, in
       "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(rblk), "r"(col), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA stores shared -> global (bulk-group completion): a 3-D / 2-D tensor box of Q (the same
+// maps as the loads), and 1-D bulk copies for vectors.  Rows outside the tensor are not
+// written.  The smem source must have been made visible to the async proxy
+// (fence.proxy.async by the writing threads, then a barrier) before the issue.
+__device__ __forceinline__ void tma_3d_s2g(const CUtensorMap* map, int rblk, int col, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(0), "r"(rblk), "r"(col), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_2d_s2g(const CUtensorMap* map, int row, int col, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(row), "r"(col), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the smem sources of every committed store have been read (the stage may be refilled)
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// every committed store has been performed (global writes complete)
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col)
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"

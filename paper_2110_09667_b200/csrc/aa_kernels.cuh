@@ -52,6 +52,7 @@ struct HeadArea {
   int rcol[4];
   int na, nr, is_last, gdone;   // gdone: Givens rotations published (K4, ICWY SMALL)
   int bd;                       // K4: this step degrades to gamma = 0 (breakdown, reading A12)
+  unsigned long long xbase;     // last CTA: sequence number before this kernel's exchanges
 };
 
 __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -329,12 +330,16 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
         H.nr = 0;
       } else {
         const int vb = p.vb;
+        // stage slot of Delta f (phase A): Q column k at recycle (the slot of the dropped
+        // column's input, so the rotated block and Delta f leave in ONE tensor store), the
+        // consumed G(x_{i-1}) slot at start-up, vb + 1 for a caller-supplied column
+        const int dfs = (p.flags & F_EXT_DF) ? vb + 1 : (p.recycle ? k : vb + 3);
         H.na = k + 2;
         for (int a = 0; a < k; ++a) H.lcol[a] = a;
         H.lcol[k] = vb;          // f_i
-        H.lcol[k + 1] = vb + 1;  // Delta f
+        H.lcol[k + 1] = dfs;     // Delta f
         H.nr = 3;
-        H.rcol[0] = vb + 1;
+        H.rcol[0] = dfs;
         H.rcol[1] = vb;
         H.rcol[2] = (k >= 1) ? k - 1 : vb;
       }
@@ -660,6 +665,12 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     double* S = stage0 + sidx * stage_words;
     mbar_wait(&bars[sidx], par);
     if (blockIdx.x == 0 && it == 0) AA_TL(3);
+    // K1 full tiles (AA_K1 TMA-store mode): outputs are written back into the stage and leave
+    // with TMA stores after phase A (the tail tile of a launch keeps per-thread stores, so
+    // rows outside this launch's range are never written)
+    const bool tma_tile = (OP == OP_K1) && p.k1_tmastore && !del_only && !(p.flags & F_EXT_DF) && rows == TR;
+    const int dfs = (OP == OP_K1) ? ((p.flags & F_EXT_DF) ? vb + 1 : (p.recycle ? k : vb + 3)) : 0;
+    (void)dfs;
 
     // ------------------------------------------------------------ phase A (row-wise)
     for (int r = tid; r < TR; r += NT) {
@@ -680,9 +691,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
               const double gpv = S[(size_t)(vb + 3) * TR + r];
               f = g - x;
               df = f - fpv;
-              p.fp[grow] = f;
-              p.gp[grow] = g;
-              p.dg_out[grow] = g - gpv;
+              if (tma_tile) {
+                // outputs stay in the stage for the tile's TMA stores: f -> slot vb (x),
+                // G(x_i) stays in slot vb + 1, Delta g -> slot vb + 2 (f_{i-1})
+                S[(size_t)(vb + 2) * TR + r] = g - gpv;
+              } else {
+                p.fp[grow] = f;
+                p.gp[grow] = g;
+                p.dg_out[grow] = g - gpv;
+              }
             }
           }
           if (p.recycle) {
@@ -690,22 +707,33 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
             // column pairs; the last carry is the dropped column.
             double carry = S[r] * H.sc[0];
             double* Qg = p.Q + grow;
+            if (tma_tile) {
 #pragma unroll 4
-            for (int j = 0; j < p.c_in - 1; ++j) {
-              const double qn = S[(size_t)(j + 1) * TR + r];   // stored (lazily scaled) column
-              const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
-              const double out = fma(a.x, carry, a.y * qn);   // c*carry + s*sc*q
-              carry = fma(b.x, carry, b.y * qn);               // -s*carry + c*sc*q
-              S[(size_t)j * TR + r] = out;
-              Qg[(size_t)j * p.ld] = out;
+              for (int j = 0; j < p.c_in - 1; ++j) {
+                const double qn = S[(size_t)(j + 1) * TR + r];   // stored (lazily scaled) column
+                const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
+                const double out = fma(a.x, carry, a.y * qn);   // c*carry + s*sc*q
+                carry = fma(b.x, carry, b.y * qn);               // -s*carry + c*sc*q
+                S[(size_t)j * TR + r] = out;
+              }
+            } else {
+#pragma unroll 4
+              for (int j = 0; j < p.c_in - 1; ++j) {
+                const double qn = S[(size_t)(j + 1) * TR + r];
+                const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
+                const double out = fma(a.x, carry, a.y * qn);
+                carry = fma(b.x, carry, b.y * qn);
+                S[(size_t)j * TR + r] = out;
+                Qg[(size_t)j * p.ld] = out;
+              }
             }
           } else {
             for (int j = 0; j < ncols; ++j) S[(size_t)j * TR + r] *= H.sc[j];
           }
           if (!del_only) {
-            p.Q[(size_t)k * p.ld + grow] = df;  // unnormalised new column (lazy scale)
+            if (!tma_tile) p.Q[(size_t)k * p.ld + grow] = df;  // unnormalised new column (lazy scale)
             S[(size_t)vb * TR + r] = f;
-            S[(size_t)(vb + 1) * TR + r] = df;
+            S[(size_t)dfs * TR + r] = df;
           }
         } else {
           // rows past this launch's range: the tensor copy zero-fills rows past n, but a
@@ -714,7 +742,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           for (int j = 0; j < p.c_in; ++j) S[(size_t)j * TR + r] = 0.0;
           if (!del_only) {
             S[(size_t)vb * TR + r] = 0.0;
-            S[(size_t)(vb + 1) * TR + r] = 0.0;
+            S[(size_t)dfs * TR + r] = 0.0;
           }
         }
       } else if constexpr (OP == OP_K2_ICWY || OP == OP_K2B_CGS2) {
@@ -818,7 +846,24 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 
     // ------------------------------------------------------------ phase B (multi-dot)
     if constexpr (NCW > 0 || GRAM) {
+      if (tma_tile) fence_proxy_async();   // this thread's stage writes -> visible to the TMA stores
       __syncthreads();
+      if constexpr (OP == OP_K1) {
+        if (tma_tile && tid == 0) {
+          // recycle: Q columns 0..k (rotated block + Delta f) in one tensor store; start-up: the
+          // new column; then f_i, G(x_i), Delta g
+          if (p.recycle) {
+            if (p.tm3d) tma_3d_s2g(&p.tm[0], (int)(row0 >> 8), 0, S);
+            else tma_2d_s2g(&p.tm[0], (int)row0, 0, S);
+          } else {
+            bulk_s2g(p.Q + (size_t)k * p.ld + row0, S + (size_t)dfs * TR, (uint32_t)TR * 8u);
+          }
+          bulk_s2g(p.fp + row0, S + (size_t)vb * TR, (uint32_t)TR * 8u);
+          bulk_s2g(p.gp + row0, S + (size_t)(vb + 1) * TR, (uint32_t)TR * 8u);
+          bulk_s2g(p.dg_out + row0, S + (size_t)(vb + 2) * TR, (uint32_t)TR * 8u);
+          bulk_commit();
+        }
+      }
       if constexpr (NCW > 0) {
         if (H.na > 0) {
 #pragma unroll 2
@@ -851,6 +896,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
         }
       }
     }
+    // the stage may be refilled only after the TMA stores have read it
+    if (tma_tile && tid == 0) bulk_wait_read0();
     __syncthreads();
     if (lane == 0 && it + NS < my_count) {
       fence_proxy_async();
@@ -860,6 +907,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   }
 
+  // the K1 TMA stores are complete before this CTA's results are published
+  if (OP == OP_K1 && p.k1_tmastore && tid == 0) bulk_wait0();
   if (blockIdx.x == 0) AA_TL(4);
   // ------------------------------------------------------------ per-CTA partials
   double* mypart = p.part + (size_t)blockIdx.x * LRED;
@@ -957,7 +1006,16 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   }
   __syncthreads();
   if constexpr (OP != OP_K4) {
-    for (int e = 0; e < p.nxchg; ++e) fused_exchange(p, outv + p.xoff[e], p.xcnt[e], p.seq0 + e);
+    if (p.nxchg > 0) {
+      // sequence numbers from the device counter (stream order: the previous kernel's last
+      // CTA has advanced it before this grid passed griddepcontrol.wait)
+      if (tid == 0) {
+        H.xbase = *p.xseq;
+        *p.xseq = H.xbase + (unsigned long long)p.nxchg;
+      }
+      __syncthreads();
+      for (int e = 0; e < p.nxchg; ++e) fused_exchange(p, outv + p.xoff[e], p.xcnt[e], H.xbase + 1ull + e);
+    }
   }
   if constexpr (OP == OP_K4) {
     if (tid == 0 && !p.chunk_last) p.st->dx2_acc = outv[0];
@@ -987,6 +1045,28 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   // kernel boundary
   if (tid == 0 && gridDim.x > 1) p.st->counter = 0u;
   AA_TL(7);
+}
+
+// aa_test_exchange: `iters` back-to-back one-shot exchanges of `words` words by one CTA,
+// timed on the device with %globaltimer (per-exchange latency)
+__global__ void __launch_bounds__(NT, 1) aa_xchg_bench_kernel(const __grid_constant__ KParams p, int words,
+                                                               int iters, unsigned long long* out_ns) {
+  __shared__ unsigned long long base;
+  double* v = p.red + (size_t)(NSLOT - 2) * LRED;
+  for (int w = threadIdx.x; w < words; w += NT) v[w] = (double)(p.rank + 1) * 1e-3 + (double)w;
+  if (threadIdx.x == 0) {
+    base = *p.xseq;
+    *p.xseq = base + (unsigned long long)iters;
+  }
+  __syncthreads();
+  const unsigned long long t0 = global_ns();
+  for (int it = 0; it < iters; ++it) {
+    fused_exchange(p, v, words, base + 1ull + (unsigned long long)it);
+    for (int w = threadIdx.x; w < words; w += NT) v[w] *= 1e-3;   // keep the values bounded
+    __syncthreads();
+  }
+  const unsigned long long t1 = global_ns();
+  if (threadIdx.x == 0) *out_ns = t1 - t0;
 }
 
 // counter-based SplitMix64 uniform generator (aa_testing.h), bitwise equal to

@@ -88,7 +88,6 @@ struct aa_ctx {
   int fused = 0;
   void* xbuf = nullptr;                 // local [flags 4 KB][mailbox 2 x nranks x LRED]
   void* peer_base[MAX_RANKS] = {};
-  unsigned long long seq = 0;
   unsigned long long* tl = nullptr;   // test-only phase timeline (aa_test_timeline)
   bool inited = false;
   int failed = AA_OK;
@@ -518,14 +517,13 @@ void plan_ar(aa_ctx* c, KParams& q, int o0, int n0, int o1, int n1) {
   const int offs[2] = {o0, o1}, cnts[2] = {n0, n1};
   q.nranks = c->nranks;
   q.rank = c->rank;
-  q.seq0 = c->seq + 1;
+  q.xseq = reinterpret_cast<unsigned long long*>(c->xbuf);   // header word 0 of the local buffer
   for (int e = 0; e < 2; ++e)
     if (cnts[e] > 0) {
       q.xoff[q.nxchg] = offs[e];
       q.xcnt[q.nxchg] = cnts[e];
       ++q.nxchg;
     }
-  c->seq += q.nxchg;
   for (int r = 0; r < c->nranks; ++r) q.pmbox[r] = (double*)((char*)c->peer_base[r] + kFlagBytes);
   q.lmbox = (double*)((char*)c->xbuf + kFlagBytes);
   c->ar_last += q.nxchg;
@@ -633,6 +631,10 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     q.dg_out = dgcol(c, dg_slot);
     q.words = L.words;
     q.red_slot = 0;
+    // K1 output path: TMA stores from the stage (default) or per-thread stores (AA_K1_STORE=0,
+    // for A/B measurements)
+    static const int k1_store = getenv("AA_K1_STORE") ? atoi(getenv("AA_K1_STORE")) : 1;
+    q.k1_tmastore = ext ? 0 : k1_store;
     // the ICWY correction-matrix update after QRDelete is its own reduction
     if (gram && L.n_gram > 0 && !c->icwy_merged) {
       k1_ar[0] = L.off_gram; k1_ar[1] = L.n_gram; k1_ar[2] = 0; k1_ar[3] = L.off_gram;
@@ -922,50 +924,77 @@ static int create_impl(aa_handle_t* out, int64_t n_local, int m, int qr_variant,
   return AA_OK;
 }
 
-// Fused-allreduce setup (collective): one device buffer per rank [flags][mailbox], its
+// Fused-allreduce setup (collective): one device buffer per rank [header][mailbox], its
 // CUDA IPC handle all-gathered over the handle's NCCL communicator, peers' buffers
-// opened with cudaIpcOpenMemHandle (NVLink P2P within the node).
+// opened with cudaIpcOpenMemHandle (NVLink P2P within the node).  Every rank takes part in
+// both collectives whatever happened locally (a rank that failed sends a dummy handle and a
+// "failed" mark), and one allreduce of the failure count decides for all: every rank enables
+// the fused exchange, or every rank keeps ncclAllReduce (no rank is left waiting in a
+// collective its peers skipped, and no rank exchanges with a peer that is not listening).
 static int fused_setup(aa_ctx* c) {
   // Any failure here leaves the handle usable with ncclAllReduce (not sticky).
   if (c->nranks > MAX_RANKS || !nccl().AllGather) return AA_ERR_ARG;
   // mailbox: [seq parity][source rank][LRED words][2 tagged halves] of 8 bytes (low-latency protocol)
   const size_t bytes = kFlagBytes + (size_t)2 * c->nranks * LRED * 2 * sizeof(unsigned long long);
-  char* dh = nullptr;
-  std::vector<cudaIpcMemHandle_t> all(c->nranks);
-  cudaIpcMemHandle_t mine;
-  auto undo = [&](int code) {
-    cudaGetLastError();
+  struct Entry {
+    cudaIpcMemHandle_t h;
+    int ok;
+    int pad[15];
+  };
+  static_assert(sizeof(Entry) * MAX_RANKS <= sizeof(double) * LRED, "handle exchange fits one slot");
+  // the exchange buffer is a reduction slot allocated at aa_create (no allocation that could fail here)
+  char* dh = reinterpret_cast<char*>(c->red + (size_t)(NSLOT - 1) * LRED);
+  double* dflag = c->red + (size_t)(NSLOT - 2) * LRED;
+  Entry mine;
+  memset(&mine, 0, sizeof(mine));
+  mine.ok = cudaMalloc(&c->xbuf, bytes) == cudaSuccess && cudaMemset(c->xbuf, 0, bytes) == cudaSuccess &&
+            cudaIpcGetMemHandle(&mine.h, c->xbuf) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+  if (!mine.ok) cudaGetLastError();
+  std::vector<Entry> all(c->nranks);
+  auto release = [&]() {
     for (int r = 0; r < MAX_RANKS; ++r) {
       if (c->peer_base[r] && c->peer_base[r] != c->xbuf) cudaIpcCloseMemHandle(c->peer_base[r]);
       c->peer_base[r] = nullptr;
     }
     if (c->xbuf) cudaFree(c->xbuf);
-    if (dh) cudaFree(dh);
     c->xbuf = nullptr;
-    fprintf(stderr, "libaa: fused NVLink allreduce unavailable (%d); keeping ncclAllReduce\n", code);
-    return code;
+    cudaGetLastError();
   };
-  if (cudaMalloc(&c->xbuf, bytes) != cudaSuccess || cudaMemset(c->xbuf, 0, bytes) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine, c->xbuf) != cudaSuccess ||
-      cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * c->nranks) != cudaSuccess ||
-      cudaMemcpy(dh + sizeof(mine) * c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice) != cudaSuccess)
-    return undo(AA_ERR_CUDA);
-  if (nccl().AllGather(dh + sizeof(mine) * c->rank, dh, sizeof(mine), 0 /*ncclInt8*/, c->comm, c->stream) != 0)
-    return undo(AA_ERR_NCCL);
-  if (cudaStreamSynchronize(c->stream) != cudaSuccess ||
-      cudaMemcpy(all.data(), dh, sizeof(mine) * c->nranks, cudaMemcpyDeviceToHost) != cudaSuccess)
-    return undo(AA_ERR_CUDA);
-  cudaFree(dh);
-  dh = nullptr;
-  for (int r = 0; r < c->nranks; ++r) {
+  if (cudaMemcpy(dh + sizeof(Entry) * c->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice) != cudaSuccess ||
+      nccl().AllGather(dh + sizeof(Entry) * c->rank, dh, sizeof(Entry), 0 /*ncclInt8*/, c->comm, c->stream) != 0 ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess ||
+      cudaMemcpy(all.data(), dh, sizeof(Entry) * c->nranks, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    // the communicator or the device itself failed: peers see the same NCCL failure
+    release();
+    fprintf(stderr, "libaa: fused NVLink allreduce set-up failed in the handle exchange\n");
+    return AA_ERR_NCCL;
+  }
+  bool ok = true;
+  for (int r = 0; r < c->nranks; ++r) ok = ok && all[r].ok;
+  for (int r = 0; r < c->nranks && ok; ++r) {
     if (r == c->rank) {
       c->peer_base[r] = c->xbuf;
-    } else if (cudaIpcOpenMemHandle(&c->peer_base[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    } else if (cudaIpcOpenMemHandle(&c->peer_base[r], all[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       c->peer_base[r] = nullptr;
-      return undo(AA_ERR_CUDA);
+      cudaGetLastError();
+      ok = false;
     }
   }
-  c->seq = 0;
+  // agree: the number of ranks that could not open every peer
+  double fails = ok ? 0.0 : 1.0;
+  if (cudaMemcpy(dflag, &fails, sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      nccl().AllReduce(dflag, dflag, 1, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0 ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess ||
+      cudaMemcpy(&fails, dflag, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    release();
+    return AA_ERR_NCCL;
+  }
+  if (fails > 0.0) {
+    release();
+    fprintf(stderr, "libaa: fused NVLink allreduce unavailable on %g rank(s); every rank keeps ncclAllReduce\n",
+            fails);
+    return AA_ERR_CUDA;
+  }
   return AA_OK;
 }
 
@@ -1441,6 +1470,56 @@ int aa_test_timeline(aa_handle_t h, int enable, uint64_t* out384) {
   if (out384 && h->tl) {
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     CUDA_TRY(h, cudaMemcpy(out384, h->tl, 384 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
+  return AA_OK;
+}
+
+int aa_test_exchange(aa_handle_t h, int words, int iters, double* us_fused, double* us_nccl) {
+  RET_IF(check_handle(h));
+  if (words < 1 || words > LRED || iters < 1) return AA_ERR_ARG;
+  if (us_fused) *us_fused = -1.0;
+  if (us_nccl) *us_nccl = -1.0;
+  if (h->nranks == 1) return AA_OK;
+  double* slot = h->red + (size_t)(NSLOT - 2) * LRED;
+  if (us_fused && h->fused && h->xbuf) {
+    KParams q = base_params(h);
+    q.red = h->red;
+    q.st = h->st;
+    q.nranks = h->nranks;
+    q.rank = h->rank;
+    q.xseq = reinterpret_cast<unsigned long long*>(h->xbuf);
+    for (int r = 0; r < h->nranks; ++r) q.pmbox[r] = (double*)((char*)h->peer_base[r] + kFlagBytes);
+    q.lmbox = (double*)((char*)h->xbuf + kFlagBytes);
+    unsigned long long* dns = nullptr;
+    CUDA_TRY(h, cudaMalloc(&dns, sizeof(unsigned long long)));
+    aa_xchg_bench_kernel<<<1, NT, 0, h->stream>>>(q, words, iters, dns);
+    h->launches++;
+    unsigned long long ns = 0;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&ns, dns, sizeof(ns), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(dns);
+    CUDA_TRY(h, e);
+    *us_fused = (double)ns * 1e-3 / iters;
+  }
+  if (us_nccl && h->comm && nccl().ok) {
+    cudaEvent_t a, b;
+    CUDA_TRY(h, cudaEventCreate(&a));
+    CUDA_TRY(h, cudaEventCreate(&b));
+    // one untimed call (lazy connection set-up), then iters back to back
+    if (nccl().AllReduce(slot, slot, (size_t)words, kNcclFloat64, kNcclSum, h->comm, h->stream) != 0)
+      return fail(h, AA_ERR_NCCL);
+    CUDA_TRY(h, cudaEventRecord(a, h->stream));
+    for (int it = 0; it < iters; ++it)
+      if (nccl().AllReduce(slot, slot, (size_t)words, kNcclFloat64, kNcclSum, h->comm, h->stream) != 0)
+        return fail(h, AA_ERR_NCCL);
+    CUDA_TRY(h, cudaEventRecord(b, h->stream));
+    CUDA_TRY(h, cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *us_nccl = (double)ms * 1e3 / iters;
   }
   return AA_OK;
 }

@@ -75,7 +75,7 @@ def test_config5b_aa_run(variant):
     # windows reach cond ~1e15 here, where the eps*kappa classes are chaotic: summation order
     # alone moves ICWY's max LOO from 0.04 to 0.8 -> compare with the summation-order envelope
     env, loos = [], []
-    for p in (1, 2, 3, 7):
+    for p in (1, 2, 3, 4, 5, 7, 8, 16, 37, 64, 148, 592):   # twelve summation orders (test_gpu_heat.py)
         r = aa_variant(lambda x: d * x + b, np.zeros(P5), M5, variant, 500, tol=1e-10, shards=p,
                        record_x=False, record_loo=True)
         if r.converged:
@@ -100,5 +100,5 @@ def test_config5b_aa_run(variant):
             break
     s.close()
     assert conv and env
-    assert min(env) - 3 <= it <= max(env) + 3, (it, env)
+    assert min(env) <= it <= max(env), (it, env)
     assert loo_max <= max(10 * max(loos), 10 * M5 * EPS * np.sqrt(N5 / 4736))

@@ -17,6 +17,13 @@ from aa_inputs.heat_torch import HeatG, dst1_lastdim  # noqa: E402
 from oracle import aa_variant  # noqa: E402
 from paper_2110_09667_b200 import aa  # noqa: E402
 
+# SURVEY.md §8(c) criteria 4 and 7: the oracle's iteration-count envelope over summation
+# orders (simulated contiguous shards summed in rank order).  Twelve orders, including the
+# GPU-like 148- and 592-way splits; profiles/r02/envelope_probe.json records the widths
+# (heat term 2: MGS 39-43, ICWY 38-42, CGS-2 39-40; Bratu 12-13) and that the GPU's count
+# falls inside with no slack.
+ENVELOPE_SHARDS = (1, 2, 3, 4, 5, 7, 8, 16, 37, 64, 148, 592)
+
 
 def test_torch_dst_matches_scipy():
     from scipy.fft import dst
@@ -62,7 +69,7 @@ def test_heat_envelope(term, m, N, variant):
     b = P.heat_rhs(N, term)
     G = lambda u: P.heat_G(u, N, term, b)
     env, sols = [], []
-    for p in (1, 2, 3, 7, 16):
+    for p in ENVELOPE_SHARDS:
         r = aa_variant(G, np.zeros(N * N), m, variant, 300, tol=tol, shards=p, record_x=False, record_loo=False,
                         breakdown="restart")
         if r.converged:
@@ -70,7 +77,7 @@ def test_heat_envelope(term, m, N, variant):
             sols.append(r.x)
     assert env, "oracle envelope empty"
     it, u = _gpu_solve(N, term, m, variant, tol, 300)
-    assert it is not None and min(env) - 2 <= it <= max(env) + 2, (it, env)
+    assert it is not None and min(env) <= it <= max(env), (it, env)
     assert min(np.linalg.norm(u - s_) for s_ in sols) <= 100 * tol
 
 
@@ -89,7 +96,7 @@ def test_bratu_envelope(variant, opts, okw):
     b = P.heat_rhs(N, 3)
     G = lambda u: P.heat_G(u, N, 3, b)
     env, sols = [], []
-    for p in (1, 2, 3, 7):
+    for p in ENVELOPE_SHARDS:
         r = aa_variant(G, np.zeros(N * N), 30, variant, 100, tol=tol, shards=p, record_x=False,
                        record_loo=False, breakdown="restart", **okw)
         if r.converged:
@@ -97,5 +104,5 @@ def test_bratu_envelope(variant, opts, okw):
             sols.append(r.x)
     assert env and max(env) < 30
     it, u = _gpu_solve(N, 3, 30, variant, tol, 100, **opts)
-    assert it is not None and min(env) - 2 <= it <= max(env) + 2, (it, env)
-    assert min(np.linalg.norm(u - s_) for s_ in sols) <= 1e3 * tol
+    assert it is not None and min(env) <= it <= max(env), (it, env)
+    assert min(np.linalg.norm(u - s_) for s_ in sols) <= 100 * tol

@@ -421,7 +421,10 @@ def test_icwy_T_is_the_gram_of_q_when_q_is_far_from_orthogonal(icwy_delete):
     start-up, ~1e-6 after recycling starts), so T's off-diagonals are far from 0 (T = I
     fails).  After every step the GPU's T rows 0..k-1 must equal the strict lower Gram of the
     GPU's own normalised columns 0..k-1 (aa_get_q; k = m_i - 1, the newest column's row is
-    formed by the next step) to 1e-12 absolute."""
+    formed by the next step) to 1e-12 absolute.  SMALL (A6b, not the paper's) propagates T
+    through the rotations instead of re-measuring it; in this regime that drifts from the
+    Gram by ~2e-8 absolute in the oracle too (cancellation: O(1) entries rotated into O(1e-7)
+    ones), so SMALL is held to 10x the oracle's own drift on the same problem."""
     n, m, iters = 20011, 20, 30
     d, b = problems.diagonal(n, 0.9, 0.99)
     dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
@@ -449,4 +452,14 @@ def test_icwy_T_is_the_gram_of_q_when_q_is_far_from_orthogonal(icwy_delete):
         assert np.all(np.diag(T[:k, :k]) == 1.0)
     s.close()
     assert biggest > 1e-2, biggest            # non-vacuous: T = I would be off by this much
-    assert worst <= 1e-12, (worst, biggest)
+    tol = 1e-12
+    if icwy_delete == "small":
+        drift = 0.0
+        for it in range(3, iters + 1):
+            r = aa_variant(lambda x: d * x + b, np.zeros(n), m, "icwy", it, icwy_delete="small",
+                           record_loo=False, record_x=False, breakdown_eps=0.0)
+            kk = r.state.mi - 1
+            Qo = r.state.Q[:, :kk]
+            drift = max(drift, float(np.max(np.abs(np.tril(r.state.T[:kk, :kk], -1) - np.tril(Qo.T @ Qo, -1)))))
+        tol = max(tol, 10 * drift)
+    assert worst <= tol, (worst, biggest, tol)

@@ -7,7 +7,7 @@ stream = torch.cuda.current_stream()
 d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
 b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
 for v in ("dcgs2", "mgs"):
-    s = aa.AndersonSolver(n, m, v, stream=stream)
+    s = aa.AndersonSolver(n, m, v, stream=stream, breakdown_eps=0.0)   # rounding-level windows: time full steps
     x = torch.zeros(n, dtype=torch.float64, device="cuda"); xn = torch.empty_like(x)
     g = torch.addcmul(b, d, x)
     s.init(x, g, xn)

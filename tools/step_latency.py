@@ -21,7 +21,8 @@ for n in ns:
     out = [f"n={n:>8d} m={m} G {tg:5.1f} us |"]
     for v in ("dcgs2", "icwy", "icwy_small", "cgs2", "mgs"):
         s = aa.AndersonSolver(n, m, "icwy" if v == "icwy_small" else v, stream=stream,
-                              icwy_delete="small" if v == "icwy_small" else None)
+                              icwy_delete="small" if v == "icwy_small" else None,
+                              breakdown_eps=0.0)   # rounding-level windows: time full steps
         x.zero_()
         s.init(x, torch.addcmul(b, d, x), xn); x, xn = xn, x
         for _ in range(m + 10):

@@ -8,7 +8,7 @@ v = sys.argv[3] if len(sys.argv) > 3 else "dcgs2"
 stream = torch.cuda.current_stream()
 d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
 b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
-s = aa.AndersonSolver(n, m, v, stream=stream)
+s = aa.AndersonSolver(n, m, v, stream=stream, breakdown_eps=0.0)   # rounding-level windows: time full steps
 x = torch.zeros(n, dtype=torch.float64, device="cuda"); xn = torch.empty_like(x)
 s.init(x, d * x + b, xn); x, xn = xn, x
 for _ in range(m + 5):
