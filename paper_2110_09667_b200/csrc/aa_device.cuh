@@ -55,6 +55,11 @@ struct Factors {
 
 struct SmallState {
   Factors f[2];
+  // QRDelete precompute, early part (written by this step's K1 spare CTA, read by its K4):
+  // rotations 0..k-3 of the next QRDelete depend only on the factor before this step's
+  // QRAdd, so they are computed while K1 streams; R' columns 0..k-3 (upper triangles)
+  double gpre_R[MMAX * MMAX];
+  double gpre_cs[MMAX], gpre_sn[MMAX];
   // ---- scalar tail (aa_stats copies only this part)
   double dx2_local;          // this rank's ||x_{i+1} - x_i||^2 from the last update
   double dx2_global;         // CONV_NORM = IMMEDIATE: the same, summed over ranks by aa_step
@@ -120,7 +125,9 @@ struct alignas(64) KParams {
   int chunk_first;  // first / last row-chunk launch of this op in the step (both 1 unchunked):
   int chunk_last;   // reductions accumulate over chunks; side effects happen once
   int pre_cta;      // K4 at small n: CTA 0 only writes the next factors + QRDelete precompute
-                    // (no tiles); tiles go to CTAs 1..gridDim-1
+                    // (no tiles); tiles go to CTAs 1..gridDim-1.  K1 at small n: CTA 0 only
+                    // computes the early rotations of the next QRDelete (k1_delete_pre)
+  int k1_pre;       // K1: compute the early rotations if a spare CTA exists; K4: K1 did (use them)
   unsigned long long* tl;   // test-only phase timeline (CTA 0 / last CTA, %globaltimer ns), or null
   int nin, tr, stages;
   int vb;           // first vector column (= sum of block columns)
@@ -272,6 +279,25 @@ constexpr int LDR = MMAX + 1;
 // hit at most two banks (they share the MIO pipe with the shuffle).
 // rho = t * t^{-1/2}, c = a t^{-1/2}, s = b t^{-1/2} with t = a^2 + b^2 after an exact
 // power-of-two scaling (one MUFU-seeded rsqrt instead of sqrt + reciprocal, no branches).
+// Givens coefficients zeroing b against a: rho = hypot(a, b) >= 0, c = a / rho, s = b / rho
+// (c = 1, s = 0 when a = b = 0).  (a, b) are scaled by an exact power of two so that
+// max(|a|,|b|) is in [1, 2): t = a'^2 + b'^2 in [1, 8) needs no over/underflow branch; one
+// rsqrt gives c, s and rho = t^{1/2} / 2^e.
+__device__ __forceinline__ void givens_coef(double a, double b, double& c, double& s, double& rho) {
+  const double mx = fmax(fabs(a), fabs(b));
+  const int ex = (__double2hiint(mx) >> 20) & 0x7ff;             // biased exponent of mx
+  const int es = ex == 0 ? 1 : (ex == 0x7ff ? 0x7fe : ex);        // zero / denormal / inf guard
+  const double sc = __hiloint2double((2046 - es) << 20, 0);       // 2^(1023 - es), exact
+  const double usc = __hiloint2double(es << 20, 0);               // 2^(es - 1023), exact
+  const double as = a * sc, bs = b * sc;
+  const double t = fma(as, as, bs * bs);
+  const bool nz = mx > 0.0;
+  const double ri = rsqrt(nz ? t : 1.0);
+  rho = nz ? (t * ri) * usc : 0.0;
+  c = nz ? as * ri : 1.0;
+  s = nz ? bs * ri : 0.0;
+}
+
 template <int LD>
 __device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn, int* progress = nullptr) {
   const int lane = threadIdx.x & 31;
@@ -288,20 +314,8 @@ __device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn, in
     const double n20 = h(j + 2, l0), n21 = h(j + 2, l1);   // next step's row j+2
     bn = (j + 1 < nc) ? R[(j + 2) + (j + 2) * LD] : 0.0;
     const double a = __shfl_sync(0xffffffffu, j < 32 ? carry0 : carry1, j & 31);
-    // scale (a, b) by an exact power of two so that max(|a|,|b|) is in [1, 2): t = a'^2 + b'^2
-    // in [1, 8) needs no over/underflow branch; one rsqrt gives c, s and rho = t^{1/2} / 2^e
-    const double mx = fmax(fabs(a), fabs(b));
-    const int ex = (__double2hiint(mx) >> 20) & 0x7ff;             // biased exponent of mx
-    const int es = ex == 0 ? 1 : (ex == 0x7ff ? 0x7fe : ex);        // zero / denormal / inf guard
-    const double sc = __hiloint2double((2046 - es) << 20, 0);       // 2^(1023 - es), exact
-    const double usc = __hiloint2double(es << 20, 0);               // 2^(es - 1023), exact
-    const double as = a * sc, bs = b * sc;
-    const double t = fma(as, as, bs * bs);
-    const bool nz = mx > 0.0;
-    const double ri = rsqrt(nz ? t : 1.0);
-    const double rho = nz ? (t * ri) * usc : 0.0;
-    const double c = nz ? as * ri : 1.0;
-    const double s = nz ? bs * ri : 0.0;
+    double c, s, rho;
+    givens_coef(a, b, c, s, rho);
     const bool act0 = l0 > j && l0 < nc, act1 = l1 > j && l1 < nc;
     const double o0 = __dadd_rn(__dmul_rn(c, carry0), __dmul_rn(s, h20));
     const double o1 = __dadd_rn(__dmul_rn(c, carry1), __dmul_rn(s, h21));

@@ -39,6 +39,17 @@ constexpr int MAXSTAGES = 8;
     }                                                                                              \
   } while (0)
 
+// the same from lane 0 of the calling warp (warp-specialised sections)
+#define AA_TLW(s)                                                                                  \
+  do {                                                                                             \
+    if (p.tl && (threadIdx.x & 31) == 0) {                                                         \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      p.tl[OP * 16 + (s)] = t_;                                                                    \
+      p.tl[128 + OP * 16 + (s)] = (unsigned long long)clock64();                                   \
+    }                                                                                              \
+  } while (0)
+
 struct HeadArea {
   double coef[NIN_MAX];
   double coef2[MMAX + 2];
@@ -52,6 +63,8 @@ struct HeadArea {
   int rcol[4];
   int na, nr, is_last, gdone;   // gdone: Givens rotations published (K4, ICWY SMALL)
   int bd;                       // K4: this step degrades to gamma = 0 (breakdown, reading A12)
+  int K4_K;                     // K4 CTA 0: columns of the new factor (warp 0 -> warp 1)
+  double K4_rkk;                // K4 CTA 0: R_kk of the new column
   unsigned long long xbase;     // last CTA: sequence number before this kernel's exchanges
 };
 
@@ -67,9 +80,44 @@ constexpr size_t SCR_V = SCR_TW + MMAX * MMAX;
 constexpr size_t SCR_R0 = SCR_V + 4 * MMAX;
 constexpr size_t SCR_RF = SCR_R0 + LRED;
 __host__ __device__ constexpr size_t scratch_bytes() { return (SCR_RF + 8) * sizeof(double); }
-// K4 with ICWY SMALL: the symmetric S of k4_tdel (m x LDR) after the scratch
-constexpr size_t SCR_S = SCR_RF + 8;
-__host__ __device__ constexpr size_t scratch_bytes_tdel(int m) { return (SCR_S + (size_t)m * LDR) * sizeof(double); }
+// K4's CTA 0: the Givens workspace Rg (copy of the new R, m x LDR), then for ICWY SMALL the
+// symmetric S of k4_tdel (m x LDR)
+constexpr size_t SCR_RG = SCR_RF + 8;
+__host__ __device__ constexpr size_t scr_s(int m) { return SCR_RG + (size_t)m * LDR; }
+__host__ __device__ constexpr size_t scratch_bytes_k4(int m, bool tdel) {
+  return (scr_s(m) + (tdel ? (size_t)m * LDR : 0)) * sizeof(double);
+}
+
+// Copy n elements src[si(e)] -> dst[di(e)], e = t0, t0 + stride, ..., with U independent loads
+// in flight per thread (all loads of a round before its stores: src and dst may both be
+// global, and a load-store loop would otherwise serialise on possible aliasing -- at small n
+// these copies sit on the step's critical path).  idx(e, si, di) maps an element.
+template <int U, class Idx>
+__device__ __forceinline__ void gather_copy(double* dst, const double* src, int n, int t0, int stride, Idx idx) {
+  for (int e0 = t0; e0 < n; e0 += stride * U) {
+    double v[U];
+    int dd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * stride;
+      dd[u] = -1;
+      if (e < n) {
+        int si, di;
+        idx(e, si, di);
+        v[u] = __ldcg(src + si);
+        dd[u] = di;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dd[u] >= 0) dst[dd[u]] = v[u];
+  }
+}
+
+// FUSED K1 (NCW <= 3, no Gram): shared memory of its end-of-kernel reduction table
+__host__ __device__ constexpr size_t fused_k1_table_bytes(int ncw) {
+  return (size_t)NT * (size_t)((3 * (8 * ncw - 2) + 3) | 1) * sizeof(double);
+}
 
 __device__ __forceinline__ double cur_scale(const KParams& p, int j) {
   // scale of stored Q column j as seen after this step's K1: rotated columns (QRDelete)
@@ -92,13 +140,27 @@ __device__ void stage_small(const KParams& p, double* scratch) {
   double* R0 = scratch + SCR_R0;
   double* RF = scratch + SCR_RF;
   const int nw = (OP == OP_K4 || OP == OP_K2_ICWY) ? p.red_words0 : 0;
-  for (int w = tid; w < nw; w += NT) R0[w] = p.red[w];
+  gather_copy<4>(R0, p.red, nw, tid, NT, [](int e, int& si, int& di) { si = e; di = e; });
   if (tid < 2) RF[tid] = p.red[(size_t)p.final_slot * LRED + tid];
   const Factors& F = p.st->f[p.ver];
   if constexpr (OP == OP_K4) {
     const double* Rsrc = p.recycle ? F.Rdel : F.R;
-    for (int j = warp; j < k; j += NWARP)
-      for (int i = lane; i < k; i += 32) Rw[i + j * LDR] = Rsrc[i + j * MMAX];
+    gather_copy<4>(Rw, Rsrc, k * k, tid, NT, [k](int e, int& si, int& di) {
+      const int j = e / k, i = e - j * k;
+      si = i + j * MMAX;
+      di = i + j * LDR;
+    });
+    // the head's other global operands, in the same round of loads: the sticky breakdown flag
+    // (RF[2]), the current scales (spare words of SCR_V) and MGS / CGS-2's R-column words
+    // from the later reduction slots (v1)
+    double* v1 = scratch + SCR_V;
+    double* scl = scratch + SCR_V + 3 * MMAX;
+    if (tid == 2) RF[2] = (double)p.st->breakdown;
+    for (int j = tid; j < p.m; j += NT) scl[j] = F.scale[j];
+    if (p.variant == V_MGS)
+      for (int j = 1 + tid; j < k; j += NT) v1[j] = p.red[(size_t)j * LRED];
+    else if (p.variant == V_CGS2)
+      for (int j = tid; j < k; j += NT) v1[j] = p.red[LRED + j];
   }
   if (p.variant == V_ICWY && (OP == OP_K4 || OP == OP_K2_ICWY)) {
     __syncthreads();   // R0 complete
@@ -124,10 +186,10 @@ struct K4Head {
   double rkk, df2;
 };
 
-// Everything Alg. 2 does after the reductions: the new R column per variant, R_kk,
-// Q^T f_i (merged into the existing reductions; A14), gamma by
-// back-substitution.  Writes Rw (K x K), Tw (ICWY), gamma into H.coef, c into cvec.
-__device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
+// Everything Alg. 2 does after the reductions, part 1: the new R column per variant, R_kk,
+// Q^T f_i (merged into the existing reductions; A14) and the breakdown test.
+// Writes Rw (K x K), c into cvec, H.bd.  Part 2 (k4_gamma): gamma by back-substitution.
+__device__ K4Head k4_rcol(const KParams& p, HeadArea& H, double* scratch) {
   const int lane = threadIdx.x & 31;
   double* Rw = scratch;                 // R' (staged by stage_small), leading dimension LDR
   double* Tw = scratch + SCR_TW;        // ICWY T' (staged)
@@ -155,8 +217,8 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
   } else {
     for (int j = lane; j < k; j += 32) {
       double r;
-      if (p.variant == V_MGS) r = (j == 0) ? red0[L.off_df] : p.red[j * LRED];
-      else if (p.variant == V_CGS2) r = red0[L.off_df + j] + p.red[LRED + j];   // s + z (Alg. 5 l.5)
+      if (p.variant == V_MGS) r = (j == 0) ? red0[L.off_df] : v1[j];            // staged red[j*LRED]
+      else if (p.variant == V_CGS2) r = red0[L.off_df + j] + v1[j];             // s + z (Alg. 5 l.5)
       else r = red0[L.off_df + j];                                               // DCGS-2 l.1 (A4)
       Rw[j + k * LDR] = r;
     }
@@ -181,19 +243,36 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
     if (lane == 0) cvec[k - 1] -= acc;
   }
   if (lane == 0) cvec[k] = vf / rkk;
-  __syncwarp();
-  for (int j = lane; j <= k; j += 32) cvec2[j] = cvec[j];
-  __syncwarp();
-  k3_back_subst<LDR>(Rw, cvec2, H.coef, k + 1);  // gamma -> H.coef[0..k]
   // breakdown (reading A12): R_kk <= eps_a ||Delta f|| (or NaN), or an
   // earlier step of this window broke down (sticky until aa_reset): the step degrades to
   // gamma = 0, x_{i+1} = G(x_i).  Every CTA (and every rank) takes the same decision: rkk
   // and ||Delta f|| are global reduction results, eps_a is the same on every rank.
-  const bool bd = !(rkk > p.eps_a * sqrt(red0[1])) || p.st->breakdown != 0;
+  const bool bd = !(rkk > p.eps_a * sqrt(red0[1])) || fin[2] != 0.0;   // fin[2]: staged st->breakdown
+  if (bd && lane == 0) H.bd = 1;
+  __syncwarp();
+  out.K = k + 1;
+  out.rkk = rkk;
+  out.df2 = red0[1];
+  return out;
+}
+
+// Part 2: gamma = R^{-1} c by back-substitution (Alg. 2 l.9) into H.coef (0 on breakdown),
+// and the damping coefficients.  Reads Rw, cvec, H.bd (one warp).
+__device__ void k4_gamma(const KParams& p, HeadArea& H, double* scratch, const K4Head& hd) {
+  const int lane = threadIdx.x & 31;
+  double* Rw = scratch;
+  double* cvec = scratch + SCR_V + MMAX;
+  double* cvec2 = cvec + MMAX;
+  const int k = p.k;
+  if (p.flags & F_DELETE_ONLY) return;
+  const double rkk = hd.rkk;
+  for (int j = lane; j <= k; j += 32) cvec2[j] = cvec[j];
+  __syncwarp();
+  k3_back_subst<LDR>(Rw, cvec2, H.coef, k + 1);  // gamma -> H.coef[0..k]
+  const bool bd = H.bd != 0;
   if (bd) {
     __syncwarp();
     for (int j = lane; j <= k; j += 32) H.coef[j] = 0.0;
-    if (lane == 0) H.bd = 1;
   }
   if (p.beta_on && !bd) {
     for (int j = lane; j <= k; j += 32) {
@@ -206,10 +285,12 @@ __device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
     if (lane == 0) H.scal[0] = 1.0 - p.beta;
   }
   __syncwarp();
-  out.K = k + 1;
-  out.rkk = rkk;
-  out.df2 = red0[1];
-  return out;
+}
+
+__device__ K4Head k4_head(const KParams& p, HeadArea& H, double* scratch) {
+  const K4Head hd = k4_rcol(p, H, scratch);
+  k4_gamma(p, H, scratch, hd);
+  return hd;
 }
 
 // The scalars the last CTA of K4 needs (R_kk and ||Delta f||^2) without the O(m^2) head.
@@ -225,20 +306,21 @@ __device__ K4Head k4_scalars_head(const KParams& p) {
   return out;
 }
 
-// CTA 0 of K4 (warp 0): write factor version ver^1 from the head's results in shared
-// memory (Rw = R_new, Tw = T'; gamma in H.coef), then precompute QRDelete(R_new) for the
-// next step: the rotations (Fo.cs/sn) and R' (Fo.Rdel), so the next
-// recycle step's heads only load them.  ICWY_DELETE = SMALL also precomputes the
-// post-delete T (k4_tdel).
+// CTA 0 of K4 writes factor version ver^1 from the head's results in shared memory and
+// precomputes QRDelete of the new R for the next step: the rotations
+// (Fo.cs/sn) and R' (Fo.Rdel), so the next recycle step's heads only load them.  Two warps
+// in parallel: warp 0 runs the serial Givens chain on a copy Rg of the new R while warp 1
+// solves for gamma and writes R, T, the scales and gamma (ICWY SMALL: warp 2 rotates T,
+// k4_tdel).
 __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K);
 
-__device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, const K4Head& hd) {
+// warp 1: R_new, T', scales, gamma -> Fo
+__device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch, int K, double rkk) {
   const int lane = threadIdx.x & 31;
   double* Rw = scratch;
   double* Tw = scratch + SCR_TW;
-  const Factors& Fi = p.st->f[p.ver];
+  const double* scl = scratch + SCR_V + 3 * MMAX;   // staged F[ver].scale
   Factors& Fo = p.st->f[p.ver ^ 1];
-  const int K = hd.K;
   const int mm = p.m;
   const bool del_only = p.flags & F_DELETE_ONLY;
   for (int j = 0; j < mm; ++j)
@@ -252,10 +334,10 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
       }
     }
   for (int j = lane; j < mm; j += 32) {
-    double s = Fi.scale[j];
+    double s = scl[j];
     if (p.recycle && j < p.k) s = 1.0;
     if (!del_only) {
-      if (j == p.k) s = 1.0 / hd.rkk;
+      if (j == p.k) s = 1.0 / rkk;
       if (p.variant == V_DCGS2 && p.reortho && j == p.k - 1) s = 1.0;
     }
     if (j >= K) s = 1.0;
@@ -264,13 +346,105 @@ __device__ void k4_write_next(const KParams& p, HeadArea& H, double* scratch, co
   }
   if (lane == 0) Fo.K = K;
   __syncwarp();
-  // QRDelete of the new R, in place in shared memory, then R' and the rotations to Fo
-  if (K >= 1) {
-    k3_givens_delete<LDR>(Rw, K, H.cs, H.sn,
-                          (p.variant == V_ICWY && p.icwy_merged == 2) ? &H.gdone : nullptr);
+}
+
+// One column of the Hessenberg matrix through rotations 0..E-1 (carry form, in place; the
+// same operations, in the same order, as k3_givens_delete applies to that column): rows
+// 0..E-1 become final, row E holds the carry.
+__device__ __forceinline__ void rotate_column(double* col, int E, const double* cs, const double* sn) {
+  double carry = col[0];
+  for (int j = 0; j < E; ++j) {
+    const double c = cs[j], s = sn[j], h2 = col[j + 1];
+    col[j] = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s, h2));
+    carry = __dadd_rn(__dmul_rn(-s, carry), __dmul_rn(c, h2));
+  }
+  col[E] = carry;
+}
+
+// warp 0: QRDelete of the new R (K = k + 1 columns), then R' and the rotations -> Fo.
+// Split form (this step's K1 had a spare CTA, p.k1_pre): rotations 0..k-3 and R' columns
+// 0..k-3 depend only on the factor before QRAdd and were computed by K1 (k1_delete_pre);
+// here only the last two columns of the Hessenberg matrix (R_new columns k-1, k) go
+// through them, and the last two rotations are formed -- bitwise the same result as the
+// full chain.  Otherwise: the full Givens chain on the copy Rg (in place).
+__device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scratch, int K) {
+  const int lane = threadIdx.x & 31;
+  double* Rw = scratch;
+  double* Rg = scratch + SCR_RG;
+  Factors& Fo = p.st->f[p.ver ^ 1];
+  const int mm = p.m;
+  const int k = K - 1;
+  int* progress = (p.variant == V_ICWY && p.icwy_merged == 2) ? &H.gdone : nullptr;
+  if (p.k1_pre && !(p.flags & F_DELETE_ONLY) && k >= 3) {
+    const int E = k - 2;
+    const SmallState* st = p.st;
+    for (int j = lane; j < E; j += 32) {
+      H.cs[j] = st->gpre_cs[j];
+      H.sn[j] = st->gpre_sn[j];
+    }
+    __syncwarp();
+    if (lane == 0 && progress) {
+      __threadfence_block();
+      *reinterpret_cast<volatile int*>(progress) = E;
+    }
+    // columns a = R_new[:, k-1] (rows 0..k; row k is 0) and b = R_new[:, k] (rows 0..k)
+    constexpr int LC = MMAX + 1;
+    double* ca = Rg;
+    double* cb = Rg + LC;
+    for (int i = lane; i <= k; i += 32) {
+      ca[i] = Rw[i + (k - 1) * LDR];
+      cb[i] = Rw[i + k * LDR];
+    }
+    __syncwarp();
+    if (lane < 2) rotate_column(lane == 0 ? ca : cb, E, H.cs, H.sn);
+    __syncwarp();
+    if (lane == 0) {
+      double c, sn_, rho;
+      givens_coef(ca[E], ca[E + 1], c, sn_, rho);      // rotation k-2: (H[k-2][k-2], R_new[k-1][k-1])
+      ca[E] = rho;
+      H.cs[E] = c;
+      H.sn[E] = sn_;
+      const double b0 = cb[E], b1 = cb[E + 1];
+      cb[E] = __dadd_rn(__dmul_rn(c, b0), __dmul_rn(sn_, b1));
+      const double carry = __dadd_rn(__dmul_rn(-sn_, b0), __dmul_rn(c, b1));
+      if (progress) {
+        __threadfence_block();
+        *reinterpret_cast<volatile int*>(progress) = E + 1;
+      }
+      givens_coef(carry, cb[E + 2], c, sn_, rho);      // rotation k-1: (H[k-1][k-1], R_kk)
+      cb[E + 1] = rho;
+      H.cs[E + 1] = c;
+      H.sn[E + 1] = sn_;
+      if (progress) {
+        __threadfence_block();
+        *reinterpret_cast<volatile int*>(progress) = E + 2;
+      }
+    }
+    __syncwarp();
+    // R' columns 0..E-1 from K1's precompute (batched loads: gpre_R and Fo.Rdel are both
+    // global), then the last two columns and the zero padding
+    gather_copy<8>(Fo.Rdel, st->gpre_R, E * E, lane, 32, [E](int e, int& si, int& di) {
+      const int j = e / E, i = e - j * E;
+      si = i + j * MMAX;
+      di = i + j * MMAX;
+    });
+    for (int j = 0; j < mm; ++j)
+      for (int i = lane; i < mm; i += 32) {
+        if (j < E && i < E) continue;   // copied above (entries below the diagonal are 0 there)
+        double v = 0.0;
+        if (i <= j && j < k) v = (j == E ? ca[i] : cb[i]);
+        Fo.Rdel[i + j * MMAX] = v;
+      }
+    for (int j = lane; j < k; j += 32) {
+      Fo.cs[j] = H.cs[j];
+      Fo.sn[j] = H.sn[j];
+    }
+    __syncwarp();
+  } else if (K >= 1) {
+    k3_givens_delete<LDR>(Rg, K, H.cs, H.sn, progress);
     for (int j = 0; j < mm; ++j)
       for (int i = lane; i < mm; i += 32)
-        Fo.Rdel[i + j * MMAX] = (i <= j && j < K - 1) ? Rw[i + j * LDR] : 0.0;
+        Fo.Rdel[i + j * MMAX] = (i <= j && j < K - 1) ? Rg[i + j * LDR] : 0.0;
     for (int j = lane; j < K - 1; j += 32) {
       Fo.cs[j] = H.cs[j];
       Fo.sn[j] = H.sn[j];
@@ -292,7 +466,7 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
   constexpr int LD = MMAX + 1;
   const int lane = threadIdx.x & 31;
   const double* Tw = scratch + SCR_TW;
-  double* S = scratch + SCR_S;   // own region (warp 0 still uses Rw for the QRDelete)
+  double* S = scratch + scr_s(p.m);   // own region (warp 0 rotates Rg meanwhile)
   const int P = K - 1;
   for (int j = 0; j < P; ++j)
     for (int i = j + lane; i < P; i += 32) {
@@ -309,6 +483,35 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
   __syncwarp();
 }
 
+// K1's spare CTA (small n): the early part of the NEXT QRDelete.  The factor before this
+// step's QRAdd is R_cur (k x k: QRDelete(R) at recycle, R at start-up); the next QRDelete
+// re-triangularises R_new[:, 1:], whose columns 1..k-2 are R_cur's, so its rotations
+// 0..k-3 and R' columns 0..k-3 are those of QRDelete of R_cur's leading (k-1) x (k-1)
+// block: computed here (one warp, scratch = this CTA's unused stage memory), finished by K4.
+__device__ void k1_delete_pre(const KParams& p, HeadArea& H, double* scratch) {
+  const int lane = threadIdx.x & 31;
+  const int k = p.k;
+  const int mold = k - 1;
+  const Factors& F = p.st->f[p.ver];
+  const double* Rsrc = p.recycle ? F.Rdel : F.R;
+  double* Rs = scratch;
+  gather_copy<8>(Rs, Rsrc, mold * mold, lane, 32, [mold](int e, int& si, int& di) {
+    const int j = e / mold, i = e - j * mold;
+    si = i + j * MMAX;
+    di = i + j * LDR;
+  });
+  __syncwarp();
+  k3_givens_delete<LDR>(Rs, mold, H.cs, H.sn, nullptr);
+  SmallState* st = p.st;
+  for (int j = 0; j < mold - 1; ++j)
+    for (int i = lane; i < mold - 1; i += 32) st->gpre_R[i + j * MMAX] = (i <= j) ? Rs[i + j * LDR] : 0.0;
+  for (int j = lane; j < mold - 1; j += 32) {
+    st->gpre_cs[j] = H.cs[j];
+    st->gpre_sn[j] = H.sn[j];
+  }
+  __syncwarp();
+}
+
 template <int OP>
 __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
   const int lane = threadIdx.x & 31;
@@ -316,14 +519,17 @@ __device__ void op_head(const KParams& p, HeadArea& H, double* scratch) {
   const int k = p.k;
   if constexpr (OP == OP_K1) {
     const Factors& F = p.st->f[p.ver];
-    for (int j = lane; j < p.c_in; j += 32) H.sc[j] = F.scale[j];
-    __syncwarp();
-    if (p.recycle)   // Givens coefficients of QRDelete(R), precomputed by the previous K4
-      for (int j = lane; j < p.c_in - 1; j += 32) {
-        const double c = F.cs[j], s = F.sn[j], scn = H.sc[j + 1];
+    // one round of independent loads: scale[j], and at recycle the Givens coefficients of
+    // QRDelete(R) precomputed by the previous K4 with the next column's scale folded in
+    for (int j = lane; j < p.c_in; j += 32) {
+      const double scj = F.scale[j];
+      H.sc[j] = scj;
+      if (p.recycle && j < p.c_in - 1) {
+        const double c = F.cs[j], s = F.sn[j], scn = F.scale[j + 1];
         H.rot[2 * j] = make_double2(c, s * scn);
         H.rot[2 * j + 1] = make_double2(-s, c * scn);
       }
+    }
     if (lane == 0) {
       if (p.flags & F_DELETE_ONLY) {
         H.na = 0;
@@ -556,6 +762,13 @@ __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned lo
 template <int OP, int NCW, int NB8>
 __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant__ KParams p) {
   constexpr bool GRAM = NB8 > 0;
+  // K1 without a Gram and with at most 22 columns (NCW <= 3): the block multi-dot is fused into
+  // the row-wise pass -- each thread keeps its rows' products with Delta f, f_i and q_{k-1} in
+  // registers (per-thread partial sums, reduced across the CTA once at the end), so the rotated
+  // columns are never written back to the stage, re-read, or separated from phase A by a
+  // barrier
+  constexpr bool FUSED = (OP == OP_K1) && !GRAM && NCW >= 1 && NCW <= 3;
+  constexpr int KMAX = FUSED ? 8 * NCW - 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + head_bytes());
@@ -588,17 +801,46 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   }
   if (blockIdx.x == 0) AA_TL(1);
   if constexpr (OP == OP_K4) {
-    if (warp == 0) {
-      hd = k4_head(p, H, scratch);
-      if (blockIdx.x == 0) AA_TL(8);
-      if (blockIdx.x == 0 && p.chunk_first) k4_write_next(p, H, scratch, hd);
-    } else if (warp == 1 && blockIdx.x == 0 && p.chunk_first && p.variant == V_ICWY && p.icwy_merged == 2) {
+    if (!(blockIdx.x == 0 && p.chunk_first)) {
+      if (warp == 0) hd = k4_head(p, H, scratch);
+    } else if (warp == 0) {
+      // the commit CTA: the new R column, then (warp 1) gamma + factor writes in parallel with
+      // (warp 0) the serial Givens QRDelete precompute of the next step
+      hd = k4_rcol(p, H, scratch);
+      if (!(p.k1_pre && !(p.flags & F_DELETE_ONLY) && p.k >= 3)) {   // full chain: on a copy of R_new
+        double* Rw = scratch;
+        double* Rg = scratch + SCR_RG;
+        for (int j = 0; j < hd.K; ++j)
+          for (int i = lane; i <= j; i += 32) Rg[i + j * LDR] = Rw[i + j * LDR];
+      }
+      if (lane == 0) {
+        H.K4_K = hd.K;
+        H.K4_rkk = hd.rkk;
+      }
+      __syncwarp();
+      asm volatile("bar.arrive 1, 64;" ::: "memory");
+      AA_TLW(8);
+      k4_delete_precompute(p, H, scratch, hd.K);
+      AA_TLW(9);
+    } else if (warp == 1) {
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+      K4Head h1{};
+      h1.K = H.K4_K;
+      h1.rkk = H.K4_rkk;
+      k4_gamma(p, H, scratch, h1);
+      AA_TLW(10);
+      k4_write_factors(p, H, scratch, h1.K, h1.rkk);
+      AA_TLW(11);
+    } else if (warp == 2 && p.variant == V_ICWY && p.icwy_merged == 2) {
       // ICWY SMALL: the post-delete T, rotated as warp 0 publishes the Givens rotations
       const int K = (p.flags & F_DELETE_ONLY) ? p.k : p.k + 1;
       if (K >= 1) k4_tdel(p, H, scratch, p.st->f[p.ver ^ 1], K);
     }
   } else {
     if (warp == 0) op_head<OP>(p, H, scratch);
+    if constexpr (OP == OP_K1) {
+      if (p.pre_cta && blockIdx.x == 0 && warp == 1) k1_delete_pre(p, H, scratch);
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], NWARP);
@@ -608,7 +850,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   if (blockIdx.x == 0) AA_TL(2);
 
   // tile CTAs: all, or (K4 pre_cta) all but CTA 0, which only did the factor precompute
-  const int pre = (OP == OP_K4) ? p.pre_cta : 0;
+  const int pre = (OP == OP_K4 || OP == OP_K1) ? p.pre_cta : 0;
   const long long tb = (long long)blockIdx.x - pre, tg = (long long)gridDim.x - pre;
   const long long my_count = (tb >= 0 && ntiles > tb) ? (ntiles - 1 - tb) / tg + 1 : 0;
   if (lane == 0) {
@@ -620,8 +862,18 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   }
 
+  // K1: CTA 0 carries the lagged ||x_i - x_{i-1}||^2 partial (A15) in its partials; load it now
+  double dx2_pref = 0.0;
+  if (OP == OP_K1 && tid == 0 && blockIdx.x == 0 && p.chunk_first && !(p.flags & (F_EXT_DF | F_DELETE_ONLY)))
+    dx2_pref = p.st->dx2_local;
   // phase-A accumulators (row-wise dots / norms)
   double a0 = 0.0, a1 = 0.0;
+  // FUSED K1: per-thread partial dots q_j . Delta f, q_j . f_i, q_j . q_{k-1}; f.f, df.df, df.f
+  double fa0[KMAX], fa1[KMAX], fa2[KMAX];
+  double fs_ff = 0.0, fs_dd = 0.0, fs_df = 0.0;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) fa0[j] = fa1[j] = fa2[j] = 0.0;
+  const bool xrhs = p.has_x && p.gram == 0;
   // phase-B accumulators: this warp's NCW columns x NRB right-hand sides
   constexpr int NRB = (OP == OP_K1) ? 3 : 1;
   constexpr int NCWx = NCW > 0 ? NCW : 1;
@@ -668,13 +920,78 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     // K1 full tiles (AA_K1 TMA-store mode): outputs are written back into the stage and leave
     // with TMA stores after phase A (the tail tile of a launch keeps per-thread stores, so
     // rows outside this launch's range are never written)
-    const bool tma_tile = (OP == OP_K1) && p.k1_tmastore && !del_only && !(p.flags & F_EXT_DF) && rows == TR;
+    const bool tma_tile = (OP == OP_K1) && !FUSED && p.k1_tmastore && !del_only && !(p.flags & F_EXT_DF) &&
+                          rows == TR;
     const int dfs = (OP == OP_K1) ? ((p.flags & F_EXT_DF) ? vb + 1 : (p.recycle ? k : vb + 3)) : 0;
     (void)dfs;
 
     // ------------------------------------------------------------ phase A (row-wise)
     for (int r = tid; r < TR; r += NT) {
       const long long grow = row0 + r;
+      if constexpr (FUSED) {
+        if (!del_only) {
+          if (r < rows) {
+            double f, df;
+            if (p.flags & F_EXT_DF) {
+              df = ldV(p, S, 0, r, rows, grow);
+              f = df;
+            } else {
+              // Alg. 1 l.3-5: f_i = G(x_i) - x_i, Delta f = f_i - f_{i-1}, Delta g = G(x_i) - G(x_{i-1})
+              const double x = ldV(p, S, 0, r, rows, grow);
+              const double g = ldV(p, S, 1, r, rows, grow);
+              const double fpv = S[(size_t)(vb + 2) * TR + r];
+              const double gpv = S[(size_t)(vb + 3) * TR + r];
+              f = g - x;
+              df = f - fpv;
+              p.fp[grow] = f;
+              p.gp[grow] = g;
+              p.dg_out[grow] = g - gpv;
+            }
+            double q[KMAX];
+            double qlast = 0.0;   // q_{k-1} of this row (no dynamic index into q: it stays in registers)
+            if (p.recycle) {
+              // QRDelete on Q: the streaming carry form of the Givens rotations (P:111,
+              // P:135-136); out_j = column j of Q' for this row, the last carry is dropped
+              double carry = S[r] * H.sc[0];
+              double* Qg = p.Q + grow;
+#pragma unroll
+              for (int j = 0; j < KMAX; ++j) {
+                q[j] = 0.0;
+                if (j < k) {
+                  const double qn = S[(size_t)(j + 1) * TR + r];
+                  const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
+                  const double out = fma(a.x, carry, a.y * qn);
+                  carry = fma(b.x, carry, b.y * qn);
+                  q[j] = out;
+                  qlast = out;
+                  Qg[(size_t)j * p.ld] = out;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < KMAX; ++j) q[j] = (j < k) ? S[(size_t)j * TR + r] * H.sc[j] : 0.0;
+              if (k >= 1) qlast = S[(size_t)(k - 1) * TR + r] * H.sc[k - 1];
+            }
+            p.Q[(size_t)k * p.ld + grow] = df;   // unnormalised new column (lazy scale)
+            // Alg. 3-6 pass 1 (Q^T Delta f, Q^T f_i and Q_{0:k-2}^T q_{k-1}) and the norms
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j)
+              if (j < k) {
+                fa0[j] = fma(q[j], df, fa0[j]);
+                fa1[j] = fma(q[j], f, fa1[j]);
+              }
+            if (xrhs) {
+#pragma unroll
+              for (int j = 0; j < KMAX; ++j)
+                if (j < k - 1) fa2[j] = fma(q[j], qlast, fa2[j]);
+            }
+            fs_ff = fma(f, f, fs_ff);
+            fs_dd = fma(df, df, fs_dd);
+            fs_df = fma(df, f, fs_df);
+          }
+          continue;
+        }
+      }
       if constexpr (OP == OP_K1) {
         const int ncols = del_only ? p.c_in : (p.recycle ? p.c_in : k);
         if (r < rows) {
@@ -845,7 +1162,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
 
     // ------------------------------------------------------------ phase B (multi-dot)
-    if constexpr (NCW > 0 || GRAM) {
+    if constexpr ((NCW > 0 && !FUSED) || GRAM) {
       if (tma_tile) fence_proxy_async();   // this thread's stage writes -> visible to the TMA stores
       __syncthreads();
       if constexpr (OP == OP_K1) {
@@ -864,7 +1181,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           bulk_commit();
         }
       }
-      if constexpr (NCW > 0) {
+      if constexpr (NCW > 0 && !FUSED) {
         if (H.na > 0) {
 #pragma unroll 2
           for (int rr = lane; rr < TR; rr += 32) {
@@ -912,16 +1229,68 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   if (blockIdx.x == 0) AA_TL(4);
   // ------------------------------------------------------------ per-CTA partials
   double* mypart = p.part + (size_t)blockIdx.x * LRED;
-  if constexpr (OP == OP_K1) {
+  if constexpr (FUSED) {
     const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
     if (!del_only) {
+      // the per-thread partials summed over the CTA in a fixed order: every thread writes its
+      // NV values to shared memory (the stage ring is idle after the tile loop; row t of an
+      // odd-strided table), then thread v sums column v over the 256 rows in four interleaved
+      // chains combined as ((c0 + c1) + (c2 + c3)) -- no shuffles (MIO-bound at small n)
+      constexpr int NV = 3 * KMAX + 3;
+      constexpr int NVP = NV | 1;
+      double* wbuf = stage0;
+      __syncthreads();
+      {
+        double* row = wbuf + (size_t)tid * NVP;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          row[j] = fa0[j];
+          row[KMAX + j] = fa1[j];
+          row[2 * KMAX + j] = fa2[j];
+        }
+        row[3 * KMAX] = fs_ff;
+        row[3 * KMAX + 1] = fs_dd;
+        row[3 * KMAX + 2] = fs_df;
+      }
+      __syncthreads();
+      for (int v = tid; v < NV; v += NT) {
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < NT; t += 4) {
+          c0 += wbuf[(size_t)t * NVP + v];
+          c1 += wbuf[(size_t)(t + 1) * NVP + v];
+          c2 += wbuf[(size_t)(t + 2) * NVP + v];
+          c3 += wbuf[(size_t)(t + 3) * NVP + v];
+        }
+        const double sum = (c0 + c1) + (c2 + c3);
+        int wd = -1;
+        if (v < KMAX) wd = (v < k) ? L.off_df + v : -1;
+        else if (v < 2 * KMAX) wd = (v - KMAX < k) ? L.off_f + (v - KMAX) : -1;
+        else if (v < 3 * KMAX) wd = (xrhs && v - 2 * KMAX < k - 1) ? L.off_x + (v - 2 * KMAX) : -1;
+        else if (v == 3 * KMAX) wd = 0;       // f.f
+        else if (v == 3 * KMAX + 1) wd = 1;   // df.df
+        else wd = 3;                          // df.f
+        if (wd >= 0) mypart[wd] = sum;
+      }
+      if (tid == 0) mypart[2] = dx2_pref;
+    }
+  } else if constexpr (OP == OP_K1) {
+    const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);
+    if (!del_only) {
+      // all NCW x NRB butterflies level by level (independent shuffles in flight together)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < NCWx; ++c)
+#pragma unroll
+          for (int b = 0; b < NRB; ++b) acc[c][b] += __shfl_xor_sync(0xffffffffu, acc[c][b], o);
 #pragma unroll
       for (int c = 0; c < NCWx; ++c) {
         const int a = warp + c * NWARP;
         if (NCW > 0 && a < H.na) {
 #pragma unroll
           for (int b = 0; b < NRB; ++b) {
-            const double v = warp_sum(acc[c][b]);
+            const double v = acc[c][b];
             if (lane == 0) {
               int w = -1;
               if (a < k) {
@@ -939,7 +1308,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
           }
         }
       }
-      if (tid == 0) mypart[2] = (blockIdx.x == 0 && p.chunk_first && !(p.flags & F_EXT_DF)) ? p.st->dx2_local : 0.0;
+      if (tid == 0) mypart[2] = dx2_pref;
     }
     if constexpr (GRAM) {
       if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, del_only ? 1 : 0, L.off_x, L.off_gram);
@@ -999,7 +1368,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   double* outv = (OP == OP_K4) ? reinterpret_cast<double*>(H.scal) + 4 : p.red + (size_t)p.red_slot * LRED;
   for (int w = tid; w < p.words; w += NT) {
     double s = 0.0;
-    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(p.part + (size_t)b * LRED + w);
+#pragma unroll 4
+    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(p.part + (size_t)b * LRED + w);   // CTA order
     // row-chunked launches (aa_step_host) add to the previous chunks' sums, in chunk order
     if (!p.chunk_first) s += (OP == OP_K4) ? (w == 0 ? p.st->dx2_acc : 0.0) : outv[w];
     outv[w] = s;

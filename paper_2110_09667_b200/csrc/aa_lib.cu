@@ -331,8 +331,8 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
     p.tm[b] = *m;
   }
   const size_t stage_bytes = (size_t)stages * align_up((size_t)nin * tr, 16) * sizeof(double);
-  const size_t scr = (OP == OP_K4 && p.variant == V_ICWY && p.icwy_merged == 2) ? scratch_bytes_tdel(p.m)
-                                                                                 : scratch_bytes();
+  size_t scr = (OP == OP_K4) ? scratch_bytes_k4(p.m, p.variant == V_ICWY && p.icwy_merged == 2) : scratch_bytes();
+  if (OP == OP_K1 && G == 0 && NCW >= 1 && NCW <= 3) scr = std::max(scr, fused_k1_table_bytes(NCW));
   const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
   // per-device state of this instance (function attributes are set per device)
   constexpr int kMaxDev = 16;
@@ -368,6 +368,16 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   if (OP == OP_K4 && ntiles >= 1 && ntiles + 1 <= (long long)c->sms * per_sm) {
     p.pre_cta = 1;
     grid = ntiles + 1;
+  }
+  // K1 when the tiles do not fill the GPU: one extra CTA (CTA 0) computes the early rotations of
+  // the next QRDelete (k1_delete_pre) while the others stream; K4 then only finishes them
+  if (OP == OP_K1) {
+    if (p.k1_pre && ntiles >= 1 && ntiles + 1 <= (long long)c->sms * per_sm) {
+      p.pre_cta = 1;
+      grid = ntiles + 1;
+    } else {
+      p.k1_pre = 0;
+    }
   }
   {
     EvScope ev(c, cls);
@@ -614,6 +624,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
 
   // ---------------- K1: prologue + QRDelete rotation + pass-1 multi-dot
   int k1_ar[4];
+  int k1_pre = 0;   // K1's spare CTA computed the early rotations of the next QRDelete
   {
     KParams q = p;
     q.op = OP_K1;
@@ -631,9 +642,10 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     q.dg_out = dgcol(c, dg_slot);
     q.words = L.words;
     q.red_slot = 0;
-    // K1 output path: TMA stores from the stage (default) or per-thread stores (AA_K1_STORE=0,
-    // for A/B measurements)
-    static const int k1_store = getenv("AA_K1_STORE") ? atoi(getenv("AA_K1_STORE")) : 1;
+    // K1 output path: per-thread coalesced stores (default) or TMA stores from the stage
+    // (AA_K1_STORE=1).  Measured A/B on B200 (profiles/r02/k1_store_ab/): equal at m = 20 and 50,
+    // 6-8 % slower at m = 5 / 10 (two CTAs per SM), so the stores stay per-thread.
+    static const int k1_store = getenv("AA_K1_STORE") ? atoi(getenv("AA_K1_STORE")) : 0;
     q.k1_tmastore = ext ? 0 : k1_store;
     // the ICWY correction-matrix update after QRDelete is its own reduction
     if (gram && L.n_gram > 0 && !c->icwy_merged) {
@@ -643,7 +655,9 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
     }
     if (!cp) {
       plan_ar(c, q, k1_ar[0], k1_ar[1], k1_ar[2], k1_ar[3]);
+      q.k1_pre = (k >= 3) ? 1 : 0;   // launch_inst keeps it only if a spare CTA exists
       RET_IF(launch_op<OP_K1>(c, q, in, 0));
+      k1_pre = q.k1_pre;
     } else {
       // row chunks: each launch waits only for its own chunk's copies; the reduction slot
       // accumulates over the chunks (in order); only the last one exchanges
@@ -718,6 +732,7 @@ int run_step(aa_ctx* c, const double* x, const double* g, double* xn, const doub
   {
     KParams q = p;
     q.op = OP_K4;
+    q.k1_pre = k1_pre;
     q.final_slot = final_slot;
     q.words = 1;
     Inputs in;

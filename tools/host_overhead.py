@@ -1,4 +1,5 @@
-"""Host-side enqueue cost of aa_step (GPU queue never drains: large backlog)."""
+"""Host-side enqueue cost of aa_step at small n (1 GPU): wall time of the aa_step call alone
+(Python binding and raw ctypes), G evaluated between calls but outside the measured span."""
 import sys, os, time, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2110_09667_b200 import aa
@@ -7,27 +8,24 @@ stream = torch.cuda.current_stream()
 d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
 b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
 for v in ("dcgs2", "mgs"):
-    s = aa.AndersonSolver(n, m, v, stream=stream, breakdown_eps=0.0)   # rounding-level windows: time full steps
+    s = aa.AndersonSolver(n, m, v, stream=stream)
     x = torch.zeros(n, dtype=torch.float64, device="cuda"); xn = torch.empty_like(x)
-    g = torch.addcmul(b, d, x)
-    s.init(x, g, xn)
+    g = torch.empty_like(x)
+    s.init(x, torch.addcmul(b, d, x), xn); x, xn = xn, x
     for _ in range(m + 5):
-        s.step(x, g, xn)
+        b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
     torch.cuda.synchronize()
     N = 300
-    t0 = time.perf_counter()
-    for _ in range(N):
-        s.step(x, g, xn)
-    t1 = time.perf_counter()
+    tpy = traw = 0.0
+    for i in range(2 * N):
+        b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g)    # the caller's G (not timed)
+        if i < N:
+            t0 = time.perf_counter(); s.step(x, g, xn); tpy += time.perf_counter() - t0
+        else:
+            t0 = time.perf_counter(); aa._lib.aa_step(s.h, x.data_ptr(), g.data_ptr(), xn.data_ptr())
+            traw += time.perf_counter() - t0
+        x, xn = xn, x
     torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    xp, gp, xnp = x.data_ptr(), g.data_ptr(), xn.data_ptr()
-    t3 = time.perf_counter()
-    for _ in range(N):
-        aa._lib.aa_step(s.h, xp, gp, xnp)
-    t4 = time.perf_counter()
-    torch.cuda.synchronize()
-    t5 = time.perf_counter()
-    print(f"{v}: python step enqueue {(t1-t0)/N*1e6:.1f} us/call, drain {(t2-t0)/N*1e6:.1f} us/iter; "
-          f"raw ctypes enqueue {(t4-t3)/N*1e6:.1f} us/call, total {(t5-t3)/N*1e6:.1f} us/iter")
+    print(f"{v}: aa_step host enqueue {tpy / N * 1e6:.1f} us/call (Python binding), "
+          f"{traw / N * 1e6:.1f} us/call (raw ctypes)")
     s.close()

@@ -10,27 +10,28 @@ stream = torch.cuda.current_stream()
 for n in ns:
     d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
     b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
+    # b is nudged every step (b += 1e-3 b), so the iteration never reaches its fixed point
+    # exactly (Delta f = 0 would be a breakdown, reading A12) and every timed step is a full one
     x = torch.zeros(n, dtype=torch.float64, device="cuda"); xn = torch.empty_like(x)
     g = torch.empty_like(x)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(20): torch.addcmul(b, d, x, out=g)
+    for _ in range(20): b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g)
     e0.record()
-    for _ in range(K): torch.addcmul(b, d, x, out=g)
+    for _ in range(K): b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g)
     e1.record(); torch.cuda.synchronize()
     tg = e0.elapsed_time(e1) / K * 1e3
     out = [f"n={n:>8d} m={m} G {tg:5.1f} us |"]
     for v in ("dcgs2", "icwy", "icwy_small", "cgs2", "mgs"):
         s = aa.AndersonSolver(n, m, "icwy" if v == "icwy_small" else v, stream=stream,
-                              icwy_delete="small" if v == "icwy_small" else None,
-                              breakdown_eps=0.0)   # rounding-level windows: time full steps
+                              icwy_delete="small" if v == "icwy_small" else None)
         x.zero_()
         s.init(x, torch.addcmul(b, d, x), xn); x, xn = xn, x
         for _ in range(m + 10):
-            torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
+            b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
         torch.cuda.synchronize()
         e0.record()
         for _ in range(K):
-            torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
+            b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
         e1.record(); torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / K * 1e3
         out.append(f"{v} {t - tg:6.1f}")

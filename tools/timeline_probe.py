@@ -8,13 +8,15 @@ v = sys.argv[3] if len(sys.argv) > 3 else "dcgs2"
 stream = torch.cuda.current_stream()
 d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
 b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
-s = aa.AndersonSolver(n, m, v, stream=stream, breakdown_eps=0.0)   # rounding-level windows: time full steps
+s = aa.AndersonSolver(n, m, v, stream=stream)
 x = torch.zeros(n, dtype=torch.float64, device="cuda"); xn = torch.empty_like(x)
 s.init(x, d * x + b, xn); x, xn = xn, x
 for _ in range(m + 5):
+    b.mul_(1.0 + 1e-3)     # never exactly at the fixed point (a breakdown would degrade the step)
     s.step(x, d * x + b, xn); x, xn = xn, x
 aa.aa_test_timeline(s.h, True)
 for _ in range(3):
+    b.mul_(1.0 + 1e-3)
     g = d * x + b
     torch.cuda.synchronize()
     s.step(x, g, xn); x, xn = xn, x
