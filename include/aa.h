@@ -123,11 +123,23 @@ enum aa_option {
                                   loop checks the norm every iteration).
                                   2 = OFF: not reported (aa_stats dx_norm = -1), no
                                   norm_check in the ledger.                                 */
-    AA_OPT_DETERMINISTIC = 9   /* reductions are always summed in a fixed order (per-CTA
-                                  partials in CTA order, ranks in rank order), so results
-                                  are bitwise reproducible for a given n_local, m, variant
-                                  and rank count; 1 (default) and 0 are both accepted and
-                                  change nothing.                                            */
+    AA_OPT_DETERMINISTIC = 9   /* 0 (default): reductions are summed in a fixed order
+                                  (per-CTA partials in CTA order, ranks in rank order), so
+                                  results are bitwise reproducible for a given n_local, m,
+                                  variant and rank count.
+                                  1: also bitwise identical ACROSS rank counts (SURVEY.md
+                                  §8(e)): every kernel sums its rows in fixed chunks of 65536
+                                  rows (one CTA per chunk, rows in a fixed order inside), the
+                                  chunk partials in a power-of-two-aligned pairwise tree over
+                                  the chunk index, and the ranks' sums in the same tree over
+                                  the rank index (fused exchange: in the kernel; NCCL: one
+                                  ncclAllGather + a summing kernel instead of ncclAllReduce).
+                                  The iterates and factors of p ranks then equal those of one
+                                  GPU bit for bit when every rank holds the same power-of-two
+                                  number of chunks.  Requires n_local % 65536 == 0 (else
+                                  AA_ERR_ARG); allocates n_local / 65536 partial slots
+                                  (AA_ERR_NOMEM).  Collective (all ranks set it).  aa_stats'
+                                  norms are still summed by ncclAllReduce.                   */
 };
 
 /* aa_stats flags */

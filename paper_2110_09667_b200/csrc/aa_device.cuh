@@ -91,6 +91,10 @@ struct K1Layout {
 };
 
 constexpr int NVEC_MAX = 8;   // 1-D vector streams per kernel
+// AA_OPT_DETERMINISTIC: rows are summed in fixed chunks of DET_ROWS rows
+// (one CTA per chunk, a fixed order inside), chunk partials in a power-of-two-aligned
+// pairwise tree over the chunk index, ranks in the same tree over the rank index
+constexpr long long DET_ROWS = 65536;
 constexpr int MAX_RANKS = 8;  // fused NVLink exchange: ranks of one node
 constexpr int NBLK_MAX = 3;   // 2-D column blocks (tensor maps) per kernel
 
@@ -158,6 +162,7 @@ struct alignas(64) KParams {
   double* red;      // reduction slots (slot s at red + s*LRED)
   double* part;     // per-CTA partials (CTA b at part + b*LRED)
   int* bd_host;     // device alias of the handle's mapped pinned breakdown word (polled by aa_step)
+  int det_tpc;      // deterministic mode: tiles per DET_ROWS chunk (CTA b = chunk b); 0 = off
 };
 
 // ------------------------------------------------------------------ PTX wrappers

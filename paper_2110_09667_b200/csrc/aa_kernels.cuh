@@ -688,6 +688,66 @@ __device__ void gram_epilogue(const KParams& p, const double* gc0, const double*
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------- deterministic sums
+// Power-of-two-aligned pairwise tree over values v(0..G-1): node (l, i) = sum of leaves
+// [i 2^l, (i+1) 2^l), a node with one missing child equals the other.  The tree depends only
+// on the leaf indices, so a rank's sum over an aligned power-of-two range of chunks is a node
+// of the global tree (bitwise identical across rank counts).
+// One warp: lane l builds the subtree of its aligned block of B leaves (binary counter),
+// then 5 shuffle levels pair aligned lane blocks.  Result valid in lane 0.
+template <class Load>
+__device__ double aligned_tree_sum_warp(int G, Load load) {
+  const int lane = threadIdx.x & 31;
+  int B = 1;
+  while (B * 32 < G) B <<= 1;
+  double stk[16];
+  int sz[16];
+  int top = 0;
+  const int base = lane * B;
+  for (int i = 0; i < B && base + i < G; ++i) {
+    double v = load(base + i);
+    int s = 1;
+    while (top > 0 && sz[top - 1] == s) {   // merge equal-size (aligned sibling) subtrees
+      v = stk[top - 1] + v;
+      s <<= 1;
+      --top;
+    }
+    stk[top] = v;
+    sz[top] = s;
+    ++top;
+  }
+  bool has = top > 0;
+  double acc = 0.0;
+  if (has) {
+    acc = stk[top - 1];
+    for (int e = top - 2; e >= 0; --e) acc = stk[e] + acc;   // missing right parts: left + (right)
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double o = __shfl_down_sync(0xffffffffu, acc, d);
+    const bool oh = __shfl_down_sync(0xffffffffu, has ? 1 : 0, d) != 0;
+    if ((lane & (2 * d - 1)) == 0) {
+      if (has && oh) acc = acc + o;
+      else if (oh) acc = o;
+      has = has || oh;
+    }
+  }
+  return acc;
+}
+
+// the same tree over R <= 8 values held by one thread (the ranks of a fused exchange)
+__device__ __forceinline__ double aligned_tree_sum_small(const double* v, int R) {
+  double t[MAX_RANKS];
+  int n = R;
+  for (int q = 0; q < R; ++q) t[q] = v[q];
+  while (n > 1) {
+    const int h = (n + 1) / 2;
+    for (int q = 0; q < h; ++q) t[q] = (2 * q + 1 < n) ? t[2 * q] + t[2 * q + 1] : t[2 * q];
+    n = h;
+  }
+  return t[0];
+}
+
 // ---------------------------------------------------------------------------- fused allreduce
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -734,6 +794,7 @@ __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned lo
   bool timed_out = false;
   for (int w = tid; w < cnt; w += NT) {
     double s = 0.0;
+    double vals[MAX_RANKS];
     for (int q = 0; q < R; ++q) {
       const unsigned long long* src = lm + ((size_t)(par * R + q) * LRED + w) * 2;
       unsigned long long lo, hi;
@@ -748,9 +809,11 @@ __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned lo
           break;
         }
       }
-      s += __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+      const double vq = __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+      vals[q] = vq;
+      s += vq;   // rank order
     }
-    v[w] = s;
+    v[w] = (p.det_tpc > 0) ? aligned_tree_sum_small(vals, R) : s;
   }
   if (timed_out) p.st->xchg_timeout = 1;
   __syncthreads();
@@ -762,12 +825,13 @@ __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned lo
 template <int OP, int NCW, int NB8>
 __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant__ KParams p) {
   constexpr bool GRAM = NB8 > 0;
-  // K1 without a Gram and with at most 22 columns (NCW <= 3): the block multi-dot is fused into
+  // K1 without a Gram and with 7..22 columns (NCW 2..3; with fewer the split form measured
+  // faster -- two CTAs per SM hide it): the block multi-dot is fused into
   // the row-wise pass -- each thread keeps its rows' products with Delta f, f_i and q_{k-1} in
   // registers (per-thread partial sums, reduced across the CTA once at the end), so the rotated
   // columns are never written back to the stage, re-read, or separated from phase A by a
   // barrier
-  constexpr bool FUSED = (OP == OP_K1) && !GRAM && NCW >= 1 && NCW <= 3;
+  constexpr bool FUSED = (OP == OP_K1) && !GRAM && NCW >= 2 && NCW <= 3;
   constexpr int KMAX = FUSED ? 8 * NCW - 2 : 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
@@ -851,8 +915,13 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 
   // tile CTAs: all, or (K4 pre_cta) all but CTA 0, which only did the factor precompute
   const int pre = (OP == OP_K4 || OP == OP_K1) ? p.pre_cta : 0;
-  const long long tb = (long long)blockIdx.x - pre, tg = (long long)gridDim.x - pre;
-  const long long my_count = (tb >= 0 && ntiles > tb) ? (ntiles - 1 - tb) / tg + 1 : 0;
+  long long tb = (long long)blockIdx.x - pre, tg = (long long)gridDim.x - pre;
+  long long my_count = (tb >= 0 && ntiles > tb) ? (ntiles - 1 - tb) / tg + 1 : 0;
+  if (p.det_tpc > 0) {   // deterministic mode: CTA b streams chunk b's tiles in order
+    tb = (long long)blockIdx.x * p.det_tpc;
+    tg = 1;
+    my_count = (ntiles > tb) ? min((long long)p.det_tpc, ntiles - tb) : 0;
+  }
   if (lane == 0) {
     fence_proxy_async();
     for (int s = 0; s < NS && s < my_count; ++s) {
@@ -1366,6 +1435,14 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   }
   AA_TL(6);   // last CTA
   double* outv = (OP == OP_K4) ? reinterpret_cast<double*>(H.scal) + 4 : p.red + (size_t)p.red_slot * LRED;
+  if (p.det_tpc > 0) {
+    // deterministic mode: the chunk partials (one per CTA) in the aligned tree, one warp per word
+    const int G = (int)gridDim.x;
+    for (int w = warp; w < p.words; w += NWARP) {
+      const double sum = aligned_tree_sum_warp(G, [&](int b) { return __ldcg(p.part + (size_t)b * LRED + w); });
+      if (lane == 0) outv[w] = sum;
+    }
+  } else
   for (int w = tid; w < p.words; w += NT) {
     double s = 0.0;
 #pragma unroll 4
@@ -1437,6 +1514,15 @@ __global__ void __launch_bounds__(NT, 1) aa_xchg_bench_kernel(const __grid_const
   }
   const unsigned long long t1 = global_ns();
   if (threadIdx.x == 0) *out_ns = t1 - t0;
+}
+
+// deterministic mode over NCCL: v[w] = aligned tree over ranks of gathered[q * cnt + w]
+__global__ void aa_det_rank_sum_kernel(double* v, const double* gathered, int cnt, int R) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < cnt; w += gridDim.x * blockDim.x) {
+    double t[MAX_RANKS];
+    for (int q = 0; q < R; ++q) t[q] = gathered[(size_t)q * cnt + w];
+    v[w] = aligned_tree_sum_small(t, R);
+  }
 }
 
 // counter-based SplitMix64 uniform generator (aa_testing.h), bitwise equal to

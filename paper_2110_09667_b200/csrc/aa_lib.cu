@@ -76,6 +76,11 @@ struct aa_ctx {
   double *red = nullptr, *part = nullptr;
   double *hx = nullptr, *hg = nullptr, *hxn = nullptr;  // staging for aa_step_host
   int* bd_host = nullptr;   // mapped pinned breakdown word (written by K4, polled by aa_step)
+  // AA_OPT_DETERMINISTIC: one partial slot per DET_ROWS chunk, and the all-gather buffer of the
+  // NCCL path (ranks summed in the aligned tree by aa_det_rank_sum_kernel)
+  int det = 0;
+  double* part_det = nullptr;
+  double* xgather = nullptr;
   int* bd_dev = nullptr;    // its device alias
   ncclComm_t comm = nullptr;
   bool own_comm = false;
@@ -267,7 +272,9 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
     CUDA_TRY(c, cudaFuncGetAttributes(&fa, aa_stream_kernel<OP, NCW, G>));
     regs = fa.numRegs;
   }
-  const bool skew = (G > 0);
+  // deterministic mode: tiles of a multiple of 256 rows dividing DET_ROWS (so every thread sees
+  // the same rows of a chunk in the same order whatever the tile), no bank-skewed Gram tiles
+  const bool skew = (G > 0) && !c->det;
   const bool vec_only = (p.nblk == 0 && p.nin > 0);
   const int nin = std::max(p.nin, 1);
   // Tile policy (tools/tune_tiles.sh sweeps, config 2, m in {5,10,20,50}):
@@ -291,8 +298,13 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   // rows when few columns let a 2-stage ring fit (m = 5 / 10: K2 3-6 % faster; m >= 20 falls
   // back to 512 rows by itself); K1 and K4 keep 512
   const bool tall = vec_only || OP == OP_K2_ICWY || OP == OP_K2_DCGS2 || OP == OP_K2B_CGS2;
+  // the fused-dot K1 (NCW 2..3, no Gram) frees its stage right after the row pass: a third
+  // stage in flight pays (m = 10: K1 3.86 -> 3.67 ms, profiles/r02/k1_tiles.txt)
+  // K1 with the ICWY Gram: bank-skewed 2-D boxes cap the tile at 252 rows, so at small m a
+  // stage is small (m = 5: 18 KB); keep up to 6 of them in flight
+  const int k1_max_stages = (OP == OP_K1 && G == 0 && NCW >= 2 && NCW <= 3) ? 3 : ((OP == OP_K1 && skew) ? 6 : 2);
   if (!k1_two && !k2a_two)
-    choose_tile(nin, skew, vec_only, 220 * 1024, 2, 2, tall ? 1024 : c->max_tr_blocks, &tr, &stages);
+    choose_tile(nin, skew, vec_only, 220 * 1024, 2, k1_max_stages, tall ? 1024 : c->max_tr_blocks, &tr, &stages);
   if (OP != OP_K1) {
     const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
     const size_t budget = (regs <= 128 && 2 * sb <= 104 * 1024) ? 104 * 1024 : 0;
@@ -303,6 +315,10 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   {
     const long long nrows = p.n - p.rbeg;
     while (!skew && !vec_only && tr >= 512 && tr % 256 == 0 && ((nrows + tr - 1) / tr) * 2 <= c->sms) tr /= 2;
+  }
+  if (c->det && tr < 256) {   // (few columns may pick taller tiles; never shorter than 256 rows)
+    tr = 256;
+    stages = 2;
   }
   // tuning override (tools only): AA_TILE="<op>:<tr>:<stages>[,<op>:<tr>:<stages>...]", read once
   static const char* const tile_override = getenv("AA_TILE");
@@ -332,7 +348,7 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   }
   const size_t stage_bytes = (size_t)stages * align_up((size_t)nin * tr, 16) * sizeof(double);
   size_t scr = (OP == OP_K4) ? scratch_bytes_k4(p.m, p.variant == V_ICWY && p.icwy_merged == 2) : scratch_bytes();
-  if (OP == OP_K1 && G == 0 && NCW >= 1 && NCW <= 3) scr = std::max(scr, fused_k1_table_bytes(NCW));
+  if (OP == OP_K1 && G == 0 && NCW >= 2 && NCW <= 3) scr = std::max(scr, fused_k1_table_bytes(NCW));
   const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
   // per-device state of this instance (function attributes are set per device)
   constexpr int kMaxDev = 16;
@@ -361,11 +377,18 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const long long ntiles = (p.n - p.rbeg + p.tr - 1) / p.tr;
   long long grid = std::min<long long>(ntiles, (long long)c->sms * per_sm);
   if (grid < 1) grid = 1;
+  p.det_tpc = 0;
+  if (c->det && p.n > 0) {   // one CTA per DET_ROWS chunk (n_local is a multiple of DET_ROWS)
+    p.det_tpc = (int)(DET_ROWS / p.tr);
+    p.part = c->part_det;
+    p.k1_pre = 0;
+    grid = (p.n - p.rbeg) / DET_ROWS;
+  }
   // K4 when the tiles do not fill the GPU: one extra CTA (CTA 0) writes the next factor
   // version and precomputes the next QRDelete while the others run gamma + the x update,
   // so that serial work leaves the kernel's critical path
   p.pre_cta = 0;
-  if (OP == OP_K4 && ntiles >= 1 && ntiles + 1 <= (long long)c->sms * per_sm) {
+  if (OP == OP_K4 && !c->det && ntiles >= 1 && ntiles + 1 <= (long long)c->sms * per_sm) {
     p.pre_cta = 1;
     grid = ntiles + 1;
   }
@@ -505,6 +528,21 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
 int allreduce(aa_ctx* c, double* buf, size_t count) {
   if (c->nranks == 1 || count == 0) return AA_OK;
   EvScope ev(c, 3);
+  if (c->det) {
+    // deterministic: all-gather the rank vectors, every rank sums them in the aligned tree
+    ncclResult_t r = nccl().AllGather(buf, c->xgather, count, kNcclFloat64, c->comm, c->stream);
+    if (r != 0) {
+      fprintf(stderr, "libaa: ncclAllGather failed: %s\n", nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+      return fail(c, AA_ERR_NCCL);
+    }
+    aa_det_rank_sum_kernel<<<(unsigned)std::max<size_t>(1, (count + 255) / 256), 256, 0, c->stream>>>(
+        buf, c->xgather, (int)count, c->nranks);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    c->ar_last++;
+    c->ar_total++;
+    return AA_OK;
+  }
   ncclResult_t r = nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, c->stream);
   if (r != 0) {
     fprintf(stderr, "libaa: ncclAllReduce failed: %s\n",
@@ -1070,7 +1108,21 @@ int aa_set_option(aa_handle_t h, int opt, double val) {
       return AA_OK;
     case AA_OPT_DETERMINISTIC:
       if (val != 0.0 && val != 1.0) return AA_ERR_ARG;
-      return AA_OK;   // always deterministic (fixed-order sums)
+      if (val == 1.0 && !h->det) {
+        // every rank's rows in whole DET_ROWS chunks (so chunks sit at the same global rows for
+        // every rank count); the chunk partials and the all-gather buffer are allocated here
+        if (h->n % DET_ROWS != 0) return AA_ERR_ARG;
+        const size_t chunks = (size_t)(h->n / DET_ROWS);
+        if (cudaMalloc(&h->part_det, sizeof(double) * LRED * chunks) != cudaSuccess ||
+            (h->nranks > 1 && cudaMalloc(&h->xgather, sizeof(double) * LRED * h->nranks) != cudaSuccess)) {
+          cudaGetLastError();
+          cudaFree(h->part_det);
+          h->part_det = nullptr;
+          return AA_ERR_NOMEM;
+        }
+      }
+      h->det = (int)val;
+      return AA_OK;
     default:
       return AA_ERR_ARG;
   }
@@ -1153,7 +1205,7 @@ int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x
       return AA_ERR_NOMEM;
     }
   }
-  if (h->n < kChunkMinRows || h->mi == 0) {
+  if (h->n < kChunkMinRows || h->mi == 0 || h->det) {
     CUDA_TRY(h, cudaMemcpyAsync(h->hx, x_i, vb, cudaMemcpyHostToDevice, h->stream));
     CUDA_TRY(h, cudaMemcpyAsync(h->hg, gx_i, vb, cudaMemcpyHostToDevice, h->stream));
     RET_IF(aa_step(h, h->hx, h->hg, h->hxn));
@@ -1404,6 +1456,8 @@ int aa_destroy(aa_handle_t h) {
   cudaFree(h->hx);
   cudaFree(h->hg);
   cudaFree(h->hxn);
+  cudaFree(h->part_det);
+  cudaFree(h->xgather);
   if (h->bd_host) cudaFreeHost(h->bd_host);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;

@@ -64,6 +64,8 @@ def test_multi_gpu_parity_and_allreduce_counts(tmp_path, mode):
         assert r["loo"] < 1e-12
         assert r["x_vs_p1"] <= 1e-13, (variant, r["x_vs_p1"])
     assert rep["breakdown_flags_identical_across_ranks"]
+    # SURVEY.md §8(e) deterministic mode: bitwise the one-GPU iterates
+    assert all(rep["deterministic_bitwise_vs_p1"].values()), rep["deterministic_bitwise_vs_p1"]
     d5, b5 = problems.diagonal(n, 0.5, 0.99)
     for variant, r in rep["breakdown"].items():
         o2 = aa_variant(lambda x: d5 * x + b5, np.zeros(n), 2, variant, 10, breakdown="restart",

@@ -463,3 +463,28 @@ def test_icwy_T_is_the_gram_of_q_when_q_is_far_from_orthogonal(icwy_delete):
             drift = max(drift, float(np.max(np.abs(np.tril(r.state.T[:kk, :kk], -1) - np.tril(Qo.T @ Qo, -1)))))
         tol = max(tol, 10 * drift)
     assert worst <= tol, (worst, biggest, tol)
+
+
+@pytest.mark.parametrize("variant,opts", [("mgs", {}), ("icwy", {}), ("icwy", {"icwy_delete": "small"}),
+                                          ("cgs2", {}), ("dcgs2", {})])
+def test_deterministic_mode(variant, opts):
+    """AA_OPT_DETERMINISTIC: rows summed in fixed 65536-row chunks, chunk
+    partials in a power-of-two-aligned pairwise tree.  Parity with the oracle (1e-10), bitwise
+    reproducible, and within rounding of the default reduction order.  (Bitwise equality across
+    rank counts: tests/test_gpu_multi.py.)"""
+    n, m, iters = 4 * 65536, 5, 14
+    d, b = problems.diagonal(n)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    okw = {"icwy_delete": "small"} if opts else {}
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, variant, iters, **okw)
+    det1 = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, iters, deterministic=1, **opts)
+    det2 = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, iters, deterministic=1, **opts)
+    dflt = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, variant, iters, **opts)
+    assert _rel_x(det1, o2, iters) <= 1e-10
+    for a, c in zip(det1.xs, det2.xs):
+        assert np.array_equal(a, c)
+    for a, c in zip(det1.xs, dflt.xs):
+        assert np.linalg.norm(a - c) <= 1e-13 * np.linalg.norm(c)
+    # the option needs whole chunks
+    with pytest.raises(aa.AAError):
+        aa.AndersonSolver(n + 256, m, variant, stream=torch.cuda.current_stream(), deterministic=1)
