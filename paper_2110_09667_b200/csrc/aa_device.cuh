@@ -314,6 +314,7 @@ __device__ void k3_givens_delete(double* R, int mold, double* cs, double* sn, in
   double h20 = h(1, l0), h21 = h(1, l1);
   double bn = (nc > 0) ? R[1 + 1 * LD] : 0.0;
   __syncwarp();
+#pragma unroll 1
   for (int j = 0; j < nc; ++j) {
     const double b = bn;                        // H[j+1][j], original
     const double n20 = h(j + 2, l0), n21 = h(j + 2, l1);   // next step's row j+2
@@ -355,6 +356,7 @@ __device__ void k3_rotate_sym(double* S, int P, const double* cs, const double* 
                               const int* progress = nullptr) {
   const int lane = threadIdx.x & 31;
   const int i0 = lane, i1 = lane + 32;
+#pragma unroll 1
   for (int j = 0; j + 1 < P; ++j) {
     if (progress) {   // rotation j is produced by another warp (k3_givens_delete)
       if (lane == 0)
@@ -404,6 +406,7 @@ __device__ void k3_forward_unit_lower(const double* T, double* r, int k) {
   const int j0 = lane, j1 = lane + 32;
   double r0 = (j0 < k) ? r[j0] : 0.0, r1 = (j1 < k) ? r[j1] : 0.0;
   double t0 = (j0 < k && k > 0) ? T[j0] : 0.0, t1 = (j1 < k && k > 0) ? T[j1] : 0.0;
+#pragma unroll 1
   for (int l = 0; l < k; ++l) {
     const double tn0 = (j0 < k && l + 1 < k) ? T[j0 + (l + 1) * MMAX] : 0.0;
     const double tn1 = (j1 < k && l + 1 < k) ? T[j1 + (l + 1) * MMAX] : 0.0;
@@ -432,6 +435,7 @@ __device__ void k3_back_subst(const double* R, double* c, double* gamma, int K) 
   const double rinv1 = (i1 < K) ? 1.0 / R[i1 + i1 * LD] : 0.0;
   double r0 = (i0 < K && K > 0) ? R[i0 + (K - 1) * LD] : 0.0;
   double r1 = (i1 < K && K > 0) ? R[i1 + (K - 1) * LD] : 0.0;
+#pragma unroll 1
   for (int j = K - 1; j >= 0; --j) {
     const double rn0 = (i0 < j && j >= 1) ? R[i0 + (j - 1) * LD] : 0.0;
     const double rn1 = (i1 < j && j >= 1) ? R[i1 + (j - 1) * LD] : 0.0;

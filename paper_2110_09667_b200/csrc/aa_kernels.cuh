@@ -94,6 +94,7 @@ __host__ __device__ constexpr size_t scratch_bytes_k4(int m, bool tdel) {
 // these copies sit on the step's critical path).  idx(e, si, di) maps an element.
 template <int U, class Idx>
 __device__ __forceinline__ void gather_copy(double* dst, const double* src, int n, int t0, int stride, Idx idx) {
+#pragma unroll 1
   for (int e0 = t0; e0 < n; e0 += stride * U) {
     double v[U];
     int dd[U];
@@ -323,6 +324,7 @@ __device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch,
   Factors& Fo = p.st->f[p.ver ^ 1];
   const int mm = p.m;
   const bool del_only = p.flags & F_DELETE_ONLY;
+#pragma unroll 1
   for (int j = 0; j < mm; ++j)
     for (int i = lane; i < mm; i += 32) {
       Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * LDR] : 0.0;
@@ -333,6 +335,8 @@ __device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch,
         Fo.T[i + j * MMAX] = v;
       }
     }
+  { constexpr int OP = OP_GRAM; AA_TLW(0); }   // (timeline detail slots of K4's commit warps)
+#pragma unroll 1
   for (int j = lane; j < mm; j += 32) {
     double s = scl[j];
     if (p.recycle && j < p.k) s = 1.0;
@@ -346,6 +350,7 @@ __device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch,
   }
   if (lane == 0) Fo.K = K;
   __syncwarp();
+  { constexpr int OP = OP_GRAM; AA_TLW(1); }
 }
 
 // One column of the Hessenberg matrix through rotations 0..E-1 (carry form, in place; the
@@ -353,6 +358,7 @@ __device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch,
 // 0..E-1 become final, row E holds the carry.
 __device__ __forceinline__ void rotate_column(double* col, int E, const double* cs, const double* sn) {
   double carry = col[0];
+#pragma unroll 1
   for (int j = 0; j < E; ++j) {
     const double c = cs[j], s = sn[j], h2 = col[j + 1];
     col[j] = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s, h2));
@@ -387,6 +393,7 @@ __device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scra
       __threadfence_block();
       *reinterpret_cast<volatile int*>(progress) = E;
     }
+    { constexpr int OP = OP_K4; AA_TLW(12); }
     // columns a = R_new[:, k-1] (rows 0..k; row k is 0) and b = R_new[:, k] (rows 0..k)
     constexpr int LC = MMAX + 1;
     double* ca = Rg;
@@ -398,6 +405,7 @@ __device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scra
     __syncwarp();
     if (lane < 2) rotate_column(lane == 0 ? ca : cb, E, H.cs, H.sn);
     __syncwarp();
+    { constexpr int OP = OP_K4; AA_TLW(13); }
     if (lane == 0) {
       double c, sn_, rho;
       givens_coef(ca[E], ca[E + 1], c, sn_, rho);      // rotation k-2: (H[k-2][k-2], R_new[k-1][k-1])
@@ -421,6 +429,7 @@ __device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scra
       }
     }
     __syncwarp();
+    { constexpr int OP = OP_K4; AA_TLW(14); }
     // R' columns 0..E-1 from K1's precompute (batched loads: gpre_R and Fo.Rdel are both
     // global), then the last two columns and the zero padding
     gather_copy<8>(Fo.Rdel, st->gpre_R, E * E, lane, 32, [E](int e, int& si, int& di) {
@@ -428,6 +437,8 @@ __device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scra
       si = i + j * MMAX;
       di = i + j * MMAX;
     });
+    { constexpr int OP = OP_K4; AA_TLW(15); }
+#pragma unroll 1
     for (int j = 0; j < mm; ++j)
       for (int i = lane; i < mm; i += 32) {
         if (j < E && i < E) continue;   // copied above (entries below the diagonal are 0 there)
@@ -435,13 +446,16 @@ __device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scra
         if (i <= j && j < k) v = (j == E ? ca[i] : cb[i]);
         Fo.Rdel[i + j * MMAX] = v;
       }
+    { constexpr int OP = OP_GRAM; AA_TLW(2); }
     for (int j = lane; j < k; j += 32) {
       Fo.cs[j] = H.cs[j];
       Fo.sn[j] = H.sn[j];
     }
     __syncwarp();
+    { constexpr int OP = OP_GRAM; AA_TLW(3); }
   } else if (K >= 1) {
     k3_givens_delete<LDR>(Rg, K, H.cs, H.sn, progress);
+#pragma unroll 1
     for (int j = 0; j < mm; ++j)
       for (int i = lane; i < mm; i += 32)
         Fo.Rdel[i + j * MMAX] = (i <= j && j < K - 1) ? Rg[i + j * LDR] : 0.0;
@@ -477,6 +491,7 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
   __syncwarp();
   k3_rotate_sym<LD>(S, P, H.cs, H.sn, &H.gdone);
   const int mm = p.m;
+#pragma unroll 1
   for (int j = 0; j < mm; ++j)
     for (int i = lane; i < mm; i += 32)
       Fo.Tdel[i + j * MMAX] = (i == j) ? 1.0 : ((j < i && i < P - 1) ? S[i + j * LD] : 0.0);
@@ -501,8 +516,11 @@ __device__ void k1_delete_pre(const KParams& p, HeadArea& H, double* scratch) {
     di = i + j * LDR;
   });
   __syncwarp();
+  { constexpr int OP = OP_K1; AA_TLW(12); }
   k3_givens_delete<LDR>(Rs, mold, H.cs, H.sn, nullptr);
+  { constexpr int OP = OP_K1; AA_TLW(13); }
   SmallState* st = p.st;
+#pragma unroll 1
   for (int j = 0; j < mold - 1; ++j)
     for (int i = lane; i < mold - 1; i += 32) st->gpre_R[i + j * MMAX] = (i <= j) ? Rs[i + j * LDR] : 0.0;
   for (int j = lane; j < mold - 1; j += 32) {
@@ -510,6 +528,7 @@ __device__ void k1_delete_pre(const KParams& p, HeadArea& H, double* scratch) {
     st->gpre_sn[j] = H.sn[j];
   }
   __syncwarp();
+  { constexpr int OP = OP_K1; AA_TLW(14); }
 }
 
 template <int OP>
@@ -874,6 +893,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       if (!(p.k1_pre && !(p.flags & F_DELETE_ONLY) && p.k >= 3)) {   // full chain: on a copy of R_new
         double* Rw = scratch;
         double* Rg = scratch + SCR_RG;
+#pragma unroll 1
         for (int j = 0; j < hd.K; ++j)
           for (int i = lane; i <= j; i += 32) Rg[i + j * LDR] = Rw[i + j * LDR];
       }
@@ -1022,18 +1042,22 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
               // QRDelete on Q: the streaming carry form of the Givens rotations (P:111,
               // P:135-136); out_j = column j of Q' for this row, the last carry is dropped
               double carry = S[r] * H.sc[0];
-              double* Qg = p.Q + grow;
+              // running pointers (one add per column instead of a 64-bit index computation)
+              double* qg = p.Q + grow;
+              const double* sp = S + TR + r;
+              const long long ld = p.ld;
 #pragma unroll
               for (int j = 0; j < KMAX; ++j) {
-                q[j] = 0.0;
-                if (j < k) {
-                  const double qn = S[(size_t)(j + 1) * TR + r];
+                if (j < k) {   // (q[j] for j >= k is never read)
+                  const double qn = *sp;
                   const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
                   const double out = fma(a.x, carry, a.y * qn);
                   carry = fma(b.x, carry, b.y * qn);
                   q[j] = out;
                   qlast = out;
-                  Qg[(size_t)j * p.ld] = out;
+                  *qg = out;
+                  qg += ld;
+                  sp += TR;
                 }
               }
             } else {
@@ -1093,6 +1117,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
             // column pairs; the last carry is the dropped column.
             double carry = S[r] * H.sc[0];
             double* Qg = p.Q + grow;
+            const long long ld = p.ld;
             if (tma_tile) {
 #pragma unroll 4
               for (int j = 0; j < p.c_in - 1; ++j) {
@@ -1103,14 +1128,17 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
                 S[(size_t)j * TR + r] = out;
               }
             } else {
+              double* sp = S + r;
 #pragma unroll 4
               for (int j = 0; j < p.c_in - 1; ++j) {
-                const double qn = S[(size_t)(j + 1) * TR + r];
+                const double qn = sp[TR];
                 const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
                 const double out = fma(a.x, carry, a.y * qn);
                 carry = fma(b.x, carry, b.y * qn);
-                S[(size_t)j * TR + r] = out;
-                Qg[(size_t)j * p.ld] = out;
+                *sp = out;
+                *Qg = out;
+                sp += TR;
+                Qg += ld;
               }
             }
           } else {

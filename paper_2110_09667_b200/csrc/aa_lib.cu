@@ -284,9 +284,10 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   // registers allow) -- small tiles (few columns) need them to keep bytes in flight.
   int tr = 0, stages = 0;
   bool k1_two = false;
-  if (OP == OP_K1 && !skew && nin < 20 && regs <= 128)
+  // (the Gram instances too when they fit: m = 10 K1 0.70 -> 0.72, m = 20 0.76 -> 0.77 of peak)
+  if (OP == OP_K1 && nin < 20 && regs <= 128)
     // K1 with few columns: keep two CTAs per SM (16 warps hide the rotation chain)
-    k1_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, c->max_tr_blocks, &tr, &stages) && tr >= 256;
+    k1_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, c->max_tr_blocks, &tr, &stages) && tr >= (skew ? 252 : 256);
   // CGS-2's K2a (phase B dots the y that phase A just produced, so a tile's two phases
   // serialise): two CTAs per SM overlap them -- the tallest tile, up to 1024 rows, whose
   // 2-stage ring lets two CTAs share an SM (sweeps: m = 20 256 rows, K2 5.34 -> 5.05 ms;
@@ -300,9 +301,9 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const bool tall = vec_only || OP == OP_K2_ICWY || OP == OP_K2_DCGS2 || OP == OP_K2B_CGS2;
   // the fused-dot K1 (NCW 2..3, no Gram) frees its stage right after the row pass: a third
   // stage in flight pays (m = 10: K1 3.86 -> 3.67 ms, profiles/r02/k1_tiles.txt)
-  // K1 with the ICWY Gram: bank-skewed 2-D boxes cap the tile at 252 rows, so at small m a
-  // stage is small (m = 5: 18 KB); keep up to 6 of them in flight
-  const int k1_max_stages = (OP == OP_K1 && G == 0 && NCW >= 2 && NCW <= 3) ? 3 : ((OP == OP_K1 && skew) ? 6 : 2);
+  // (K1 with the ICWY Gram: up to 6 stages of its 252-row tiles measured slower -- m = 10
+  // 0.69 -> 0.50, m = 20 0.77 -> 0.59 of peak -- so it keeps 2)
+  const int k1_max_stages = (OP == OP_K1 && G == 0 && NCW >= 2 && NCW <= 3) ? 3 : 2;
   if (!k1_two && !k2a_two)
     choose_tile(nin, skew, vec_only, 220 * 1024, 2, k1_max_stages, tall ? 1024 : c->max_tr_blocks, &tr, &stages);
   if (OP != OP_K1) {

@@ -20,13 +20,14 @@ def _expand(name):
 
 def test_cited_evidence_files_exist():
     missing = []
-    for md, base in (("profiles/README.md", "profiles/r01"), ("README.md", ""), ("DESIGN.md", "")):
+    for md, base in (("profiles/README.md", "profiles/r02"), ("profiles/r01/README.md", "profiles/r01"),
+                     ("README.md", ""), ("DESIGN.md", "")):
         for name in _cited(md):
             if "*" in name or name in ("SPEC.md", "PAPER.md"):   # the reference's own documents
                 continue
             for n in _expand(name):
-                dirs = ("", base, "profiles", "profiles/r01", "tools", "tests", "include", "oracle", "aa_inputs",
-                        "paper_2110_09667_b200", "paper_2110_09667_b200/csrc")
+                dirs = ("", base, "profiles", "profiles/r01", "profiles/r01/history", "profiles/r02", "tools", "tests",
+                        "include", "oracle", "aa_inputs", "paper_2110_09667_b200", "paper_2110_09667_b200/csrc")
                 candidates = [os.path.join(ROOT, d, n) for d in dirs]
                 if not any(os.path.exists(c) for c in candidates):
                     missing.append((md, n))

@@ -131,7 +131,8 @@ def _full_one(d, name, tag):
             "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__shared_mem_per_block_dynamic"]
-    lines = [f"# {tag}: `ncu --set full` of {name} (n_local = 2e7, m = 20, recycle): "
+    size = {"k1_icwy50": "n_local = 2e7, m = 50", "k1_dcgs2": "n_local = 1e8, m = 20" if tag != "r01" else "n_local = 2e7, m = 20"}.get(name, "n_local = 2e7, m = 20")
+    lines = [f"# {tag}: `ncu --set full` of {name} ({size}, recycle): "
              f"{d.get('Kernel Name', '')[:60]}", "", "| metric | value |", "|---|---|"]
     for kk in keys:
         if kk in d:
@@ -157,10 +158,10 @@ def main():
             "(single pass), averaged over the 3 timed steps.  algorithmic = DESIGN.md §7 byte model.", "",
             "| kernel | DRAM GB/launch | algorithmic GB | ratio | ncu ms | ncu GB/s |", "|---|---|---|---|---|---|"]
     r1, t_d = traffic(src, "traffic.csv", 20, "dcgs2")
-    r2, t_i = traffic(src, "traffic_icwy.csv", 20, "icwy")
+    r2, t_i = traffic(src, "traffic_icwy.csv", 20, "icwy") if os.path.exists(os.path.join(src, "traffic_icwy.csv")) else ([], {})
     r3 = traffic(src, "traffic_cgs2.csv", 20, "cgs2")[0] if os.path.exists(os.path.join(src, "traffic_cgs2.csv")) else []
     open(os.path.join(dst, "traffic.md"), "w").write("\n".join(rows + r1 + r2 + r3) + "\n")
-    for name in ("k1_dcgs2", "k1_icwy", "k2_cgs2"):
+    for name in ("k1_dcgs2", "k1_icwy", "k2_cgs2", "k1_icwy50"):
         if os.path.exists(os.path.join(src, name + ".ncu-rep")):
             open(os.path.join(dst, name + ".md"), "w").write(full(src, name, tag) + "\n")
     summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")

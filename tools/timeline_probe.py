@@ -23,6 +23,8 @@ for _ in range(3):
     tlc = aa.aa_test_timeline(s.h, True).astype(np.int64)
     tl, ck = tlc[0], tlc[1]
 names = ["entry", "staged", "head", "tile0", "tiles", "partials", "red", "end"]
+# (slots of op 7 carry K4 commit-warp details; the LOO Gram kernel is not run here)
+det = [(i, int(tl[7, i]), int(ck[7, i])) for i in range(4) if tl[7, i] > 0]
 ops = {0: "K1", 1: "K2icwy", 2: "K2dcgs2", 3: "K2a", 4: "K2b", 5: "K2mgs", 6: "K4"}
 t0 = min(int(tl[o, 0]) for o in ops if tl[o, 0] > 0)
 for o, nm in ops.items():
@@ -32,7 +34,12 @@ for o, nm in ops.items():
     sub = [(i, int(tl[o, i]) - t0) for i in range(8, 16) if tl[o, i] > 0]
     if sub:
         print("         sub:", " ".join(f"[{i}]={v/1e3:7.2f}" for i, v in sub))
+        # clock64 of the same marks (CTA 0 slots share an SM): cycles after the head mark
+        c2 = int(ck[o, 2])
+        print("         sub cycles after 'staged':", " ".join(f"[{i}]={int(ck[o, i]) - int(ck[o, 1])}" for i, _ in sub))
     # effective SM clock from clock64 deltas (CTA 0 slots 0..5 are on one SM)
     dt = tl[o, 5] - tl[o, 0]; dc = ck[o, 5] - ck[o, 0]
     if dt > 0: print(f"         SM clock over entry..partials: {dc / dt * 1e3:.0f} MHz ({dc} cycles)")
-
+if det:
+    print("K4 commit detail (0 R/T stores done, 1 scale/gamma stores done, 2 Rdel stores done, 3 cs/sn done):",
+          " ".join(f"[{i}]={(t - t0) / 1e3:.2f}us/{c - int(ck[6, 1])}cyc" for i, t, c in det))
