@@ -404,7 +404,7 @@ def main():
                "startup_ms_total": max_over_ranks(startup_ms), "startup_iters": m}
         e2e_res = None
         if e2e:
-            nh = 3
+            nh = 10
             # all three host buffers pinned (empty_like does not inherit pinning)
             xh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
             gh = torch.empty(n_local, dtype=torch.float64, pin_memory=True)

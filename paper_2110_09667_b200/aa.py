@@ -12,7 +12,8 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaa.so")
+# AA_LIB: an alternative in-tree build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("AA_LIB") or os.path.join(HERE, "libaa.so")
 
 MGS, ICWY, CGS2, DCGS2 = 0, 1, 2, 3
 VARIANT_IDS = {"mgs": MGS, "icwy": ICWY, "cgs2": CGS2, "dcgs2": DCGS2}

@@ -196,7 +196,6 @@ __device__ K4Head k4_rcol(const KParams& p, HeadArea& H, double* scratch) {
   double* Tw = scratch + SCR_TW;        // ICWY T' (staged)
   double* v1 = scratch + SCR_V;         // MMAX words
   double* cvec = v1 + MMAX;             // MMAX
-  double* cvec2 = cvec + MMAX;          // MMAX
   const double* red0 = scratch + SCR_R0;
   const double* fin = scratch + SCR_RF;
   const int k = p.k;
@@ -315,27 +314,36 @@ __device__ K4Head k4_scalars_head(const KParams& p) {
 // k4_tdel).
 __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors& Fo, int K);
 
-// warp 1: R_new, T', scales, gamma -> Fo
+// The commit CTA's store warps (3..7, `nt` threads from `t0`): R_new and T' -> Fo, as soon as
+// warp 0 has formed R_new (they are independent of gamma); one flattened pass, so the
+// stores of all five warps are in flight together (a one-warp loop of dependent
+// iterations cost ~300 cycles per column at small n)
+__device__ void k4_store_RT(const KParams& p, double* scratch, int K, int t0, int nt) {
+  const double* Rw = scratch;
+  const double* Tw = scratch + SCR_TW;
+  Factors& Fo = p.st->f[p.ver ^ 1];
+  const int mm = p.m;
+  const bool icwy = p.variant == V_ICWY;
+#pragma unroll 1
+  for (int e = t0; e < mm * mm; e += nt) {
+    const int jj = e / mm, ii = e - jj * mm;
+    Fo.R[ii + jj * MMAX] = (ii < K && jj < K) ? Rw[ii + jj * LDR] : 0.0;
+    if (icwy) {
+      double v = 0.0;
+      if (ii == jj) v = (ii < K) ? 1.0 : 0.0;
+      else if (jj < ii && ii < p.k) v = Tw[ii + jj * MMAX];
+      Fo.T[ii + jj * MMAX] = v;
+    }
+  }
+}
+
+// warp 1: scales, gamma, K -> Fo
 __device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch, int K, double rkk) {
   const int lane = threadIdx.x & 31;
-  double* Rw = scratch;
-  double* Tw = scratch + SCR_TW;
   const double* scl = scratch + SCR_V + 3 * MMAX;   // staged F[ver].scale
   Factors& Fo = p.st->f[p.ver ^ 1];
   const int mm = p.m;
   const bool del_only = p.flags & F_DELETE_ONLY;
-#pragma unroll 1
-  for (int j = 0; j < mm; ++j)
-    for (int i = lane; i < mm; i += 32) {
-      Fo.R[i + j * MMAX] = (i < K && j < K) ? Rw[i + j * LDR] : 0.0;
-      if (p.variant == V_ICWY) {
-        double v = 0.0;
-        if (i == j) v = (i < K) ? 1.0 : 0.0;
-        else if (j < i && i < p.k) v = Tw[i + j * MMAX];
-        Fo.T[i + j * MMAX] = v;
-      }
-    }
-  { constexpr int OP = OP_GRAM; AA_TLW(0); }   // (timeline detail slots of K4's commit warps)
 #pragma unroll 1
   for (int j = lane; j < mm; j += 32) {
     double s = scl[j];
@@ -350,7 +358,6 @@ __device__ void k4_write_factors(const KParams& p, HeadArea& H, double* scratch,
   }
   if (lane == 0) Fo.K = K;
   __syncwarp();
-  { constexpr int OP = OP_GRAM; AA_TLW(1); }
 }
 
 // One column of the Hessenberg matrix through rotations 0..E-1 (carry form, in place; the
@@ -367,21 +374,24 @@ __device__ __forceinline__ void rotate_column(double* col, int E, const double* 
   col[E] = carry;
 }
 
-// warp 0: QRDelete of the new R (K = k + 1 columns), then R' and the rotations -> Fo.
+// warp 0: QRDelete of the new R (K = k + 1 columns): the rotations into H.cs / H.sn and R' in
+// shared memory (the commit CTA's store warps write them out afterwards, k4_delete_store).
 // Split form (this step's K1 had a spare CTA, p.k1_pre): rotations 0..k-3 and R' columns
 // 0..k-3 depend only on the factor before QRAdd and were computed by K1 (k1_delete_pre);
 // here only the last two columns of the Hessenberg matrix (R_new columns k-1, k) go
 // through them, and the last two rotations are formed -- bitwise the same result as the
 // full chain.  Otherwise: the full Givens chain on the copy Rg (in place).
-__device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scratch, int K) {
+__device__ __forceinline__ bool k4_split(const KParams& p, int K) {
+  return p.k1_pre && !(p.flags & F_DELETE_ONLY) && K - 1 >= 3;
+}
+
+__device__ void k4_delete_compute(const KParams& p, HeadArea& H, double* scratch, int K) {
   const int lane = threadIdx.x & 31;
   double* Rw = scratch;
   double* Rg = scratch + SCR_RG;
-  Factors& Fo = p.st->f[p.ver ^ 1];
-  const int mm = p.m;
   const int k = K - 1;
   int* progress = (p.variant == V_ICWY && p.icwy_merged == 2) ? &H.gdone : nullptr;
-  if (p.k1_pre && !(p.flags & F_DELETE_ONLY) && k >= 3) {
+  if (k4_split(p, K)) {
     const int E = k - 2;
     const SmallState* st = p.st;
     for (int j = lane; j < E; j += 32) {
@@ -429,44 +439,49 @@ __device__ void k4_delete_precompute(const KParams& p, HeadArea& H, double* scra
       }
     }
     __syncwarp();
-    { constexpr int OP = OP_K4; AA_TLW(14); }
-    // R' columns 0..E-1 from K1's precompute (batched loads: gpre_R and Fo.Rdel are both
-    // global), then the last two columns and the zero padding
-    gather_copy<8>(Fo.Rdel, st->gpre_R, E * E, lane, 32, [E](int e, int& si, int& di) {
-      const int j = e / E, i = e - j * E;
-      si = i + j * MMAX;
-      di = i + j * MMAX;
-    });
-    { constexpr int OP = OP_K4; AA_TLW(15); }
-#pragma unroll 1
-    for (int j = 0; j < mm; ++j)
-      for (int i = lane; i < mm; i += 32) {
-        if (j < E && i < E) continue;   // copied above (entries below the diagonal are 0 there)
-        double v = 0.0;
-        if (i <= j && j < k) v = (j == E ? ca[i] : cb[i]);
-        Fo.Rdel[i + j * MMAX] = v;
-      }
-    { constexpr int OP = OP_GRAM; AA_TLW(2); }
-    for (int j = lane; j < k; j += 32) {
-      Fo.cs[j] = H.cs[j];
-      Fo.sn[j] = H.sn[j];
-    }
-    __syncwarp();
-    { constexpr int OP = OP_GRAM; AA_TLW(3); }
   } else if (K >= 1) {
     k3_givens_delete<LDR>(Rg, K, H.cs, H.sn, progress);
-#pragma unroll 1
-    for (int j = 0; j < mm; ++j)
-      for (int i = lane; i < mm; i += 32)
-        Fo.Rdel[i + j * MMAX] = (i <= j && j < K - 1) ? Rg[i + j * LDR] : 0.0;
-    for (int j = lane; j < K - 1; j += 32) {
-      Fo.cs[j] = H.cs[j];
-      Fo.sn[j] = H.sn[j];
-    }
-    __syncwarp();
   }
-  if (lane == 0) Fo.has_del = 1;
-  __syncwarp();
+  { constexpr int OP = OP_K4; AA_TLW(14); }
+}
+
+// The store warps: R' and the rotations -> Fo.  Part 1 (before the Givens results): in the
+// split form, R' columns 0..k-3 straight from K1's precompute.  Part 2 (after): the rest.
+__device__ void k4_delete_store_early(const KParams& p, int K, int t0, int nt) {
+  if (!k4_split(p, K)) return;
+  const int E = K - 3;
+  Factors& Fo = p.st->f[p.ver ^ 1];
+  gather_copy<4>(Fo.Rdel, p.st->gpre_R, E * E, t0, nt, [E](int e, int& si, int& di) {
+    const int j = e / E, i = e - j * E;
+    si = i + j * MMAX;
+    di = i + j * MMAX;
+  });
+}
+
+__device__ void k4_delete_store(const KParams& p, HeadArea& H, double* scratch, int K, int t0, int nt) {
+  const double* Rg = scratch + SCR_RG;
+  Factors& Fo = p.st->f[p.ver ^ 1];
+  const int mm = p.m;
+  const int k = K - 1;
+  const bool split = k4_split(p, K);
+  const int E = k - 2;
+  constexpr int LC = MMAX + 1;
+#pragma unroll 1
+  for (int e = t0; e < mm * mm; e += nt) {
+    const int j = e / mm, i = e - j * mm;
+    double v = 0.0;
+    if (split) {
+      if (j < E && i < E) continue;   // written by k4_delete_store_early (zeros below the diagonal)
+      if (i <= j && j < k) v = (j == E) ? Rg[i] : Rg[LC + i];
+    } else if (K >= 1) {
+      if (i <= j && j < K - 1) v = Rg[i + j * LDR];
+    }
+    Fo.Rdel[i + j * MMAX] = v;
+  }
+  for (int j = t0; j < K - 1; j += nt) {
+    Fo.cs[j] = H.cs[j];
+    Fo.sn[j] = H.sn[j];
+  }
 }
 
 // ICWY_DELETE = SMALL (variant, not in the paper, A6b):
@@ -504,31 +519,40 @@ __device__ void k4_tdel(const KParams& p, HeadArea& H, double* scratch, Factors&
 // 0..k-3 and R' columns 0..k-3 are those of QRDelete of R_cur's leading (k-1) x (k-1)
 // block: computed here (one warp, scratch = this CTA's unused stage memory), finished by K4.
 __device__ void k1_delete_pre(const KParams& p, HeadArea& H, double* scratch) {
-  const int lane = threadIdx.x & 31;
+  // warps 1..7 of the spare CTA (224 threads; warp 0 runs the op head): stage R_cur together,
+  // warp 1 runs the serial Givens chain, all seven write the results (one warp's dependent
+  // store loop costs ~300 cycles per column at small n)
+  const int t = threadIdx.x - 32, nt = NT - 32;
+  const int warp = threadIdx.x >> 5;
   const int k = p.k;
   const int mold = k - 1;
   const Factors& F = p.st->f[p.ver];
   const double* Rsrc = p.recycle ? F.Rdel : F.R;
   double* Rs = scratch;
-  gather_copy<8>(Rs, Rsrc, mold * mold, lane, 32, [mold](int e, int& si, int& di) {
+  gather_copy<4>(Rs, Rsrc, mold * mold, t, nt, [mold](int e, int& si, int& di) {
     const int j = e / mold, i = e - j * mold;
     si = i + j * MMAX;
     di = i + j * LDR;
   });
-  __syncwarp();
-  { constexpr int OP = OP_K1; AA_TLW(12); }
-  k3_givens_delete<LDR>(Rs, mold, H.cs, H.sn, nullptr);
-  { constexpr int OP = OP_K1; AA_TLW(13); }
+  asm volatile("bar.sync 3, 224;" ::: "memory");
+  if (warp == 1) {
+    { constexpr int OP = OP_K1; AA_TLW(12); }
+    k3_givens_delete<LDR>(Rs, mold, H.cs, H.sn, nullptr);
+    { constexpr int OP = OP_K1; AA_TLW(13); }
+  }
+  asm volatile("bar.sync 3, 224;" ::: "memory");
   SmallState* st = p.st;
+  const int E = mold - 1;
 #pragma unroll 1
-  for (int j = 0; j < mold - 1; ++j)
-    for (int i = lane; i < mold - 1; i += 32) st->gpre_R[i + j * MMAX] = (i <= j) ? Rs[i + j * LDR] : 0.0;
-  for (int j = lane; j < mold - 1; j += 32) {
+  for (int e = t; e < E * E; e += nt) {
+    const int j = e / E, i = e - j * E;
+    st->gpre_R[i + j * MMAX] = (i <= j) ? Rs[i + j * LDR] : 0.0;
+  }
+  for (int j = t; j < E; j += nt) {
     st->gpre_cs[j] = H.cs[j];
     st->gpre_sn[j] = H.sn[j];
   }
-  __syncwarp();
-  { constexpr int OP = OP_K1; AA_TLW(14); }
+  if (warp == 1) { constexpr int OP = OP_K1; AA_TLW(14); }
 }
 
 template <int OP>
@@ -852,6 +876,10 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   // barrier
   constexpr bool FUSED = (OP == OP_K1) && !GRAM && NCW >= 2 && NCW <= 3;
   constexpr int KMAX = FUSED ? 8 * NCW - 2 : 1;
+  // per-column guards on the fused dots: measured A/B (profiles/r02/k1_fused_variants_ab.txt):
+  // guarded is 6 % faster at NCW = 3 (m = 20), unguarded (zeros past k, no selects) 3 %
+  // faster at NCW = 2 (m = 10)
+  constexpr bool GUARD = (NCW == 3);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + head_bytes());
@@ -887,10 +915,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     if (!(blockIdx.x == 0 && p.chunk_first)) {
       if (warp == 0) hd = k4_head(p, H, scratch);
     } else if (warp == 0) {
-      // the commit CTA: the new R column, then (warp 1) gamma + factor writes in parallel with
-      // (warp 0) the serial Givens QRDelete precompute of the next step
+      // the commit CTA: warp 0 forms the new R column, then runs the serial Givens chain of the
+      // next QRDelete; warp 1 (released by named barrier 1) solves gamma and writes the scales;
+      // warps 3..7 write R and T (barrier 1) and R' and the rotations (barrier 2) in parallel
       hd = k4_rcol(p, H, scratch);
-      if (!(p.k1_pre && !(p.flags & F_DELETE_ONLY) && p.k >= 3)) {   // full chain: on a copy of R_new
+      if (!k4_split(p, hd.K)) {   // full chain: on a copy of R_new
         double* Rw = scratch;
         double* Rg = scratch + SCR_RG;
 #pragma unroll 1
@@ -902,12 +931,13 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
         H.K4_rkk = hd.rkk;
       }
       __syncwarp();
-      asm volatile("bar.arrive 1, 64;" ::: "memory");
+      asm volatile("bar.arrive 1, 224;" ::: "memory");
       AA_TLW(8);
-      k4_delete_precompute(p, H, scratch, hd.K);
+      k4_delete_compute(p, H, scratch, hd.K);
+      asm volatile("bar.arrive 2, 192;" ::: "memory");
       AA_TLW(9);
     } else if (warp == 1) {
-      asm volatile("bar.sync 1, 64;" ::: "memory");
+      asm volatile("bar.sync 1, 224;" ::: "memory");
       K4Head h1{};
       h1.K = H.K4_K;
       h1.rkk = H.K4_rkk;
@@ -915,6 +945,16 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       AA_TLW(10);
       k4_write_factors(p, H, scratch, h1.K, h1.rkk);
       AA_TLW(11);
+    } else if (warp >= 3) {
+      asm volatile("bar.sync 1, 224;" ::: "memory");
+      const int K = H.K4_K;
+      const int t3 = tid - 96;
+      k4_store_RT(p, scratch, K, t3, NT - 96);
+      k4_delete_store_early(p, K, t3, NT - 96);
+      if (warp == 3) { AA_TLW(15); }
+      asm volatile("bar.sync 2, 192;" ::: "memory");
+      k4_delete_store(p, H, scratch, K, t3, NT - 96);
+      if (t3 == 0) p.st->f[p.ver ^ 1].has_del = 1;
     } else if (warp == 2 && p.variant == V_ICWY && p.icwy_merged == 2) {
       // ICWY SMALL: the post-delete T, rotated as warp 0 publishes the Givens rotations
       const int K = (p.flags & F_DELETE_ONLY) ? p.k : p.k + 1;
@@ -923,7 +963,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   } else {
     if (warp == 0) op_head<OP>(p, H, scratch);
     if constexpr (OP == OP_K1) {
-      if (p.pre_cta && blockIdx.x == 0 && warp == 1) k1_delete_pre(p, H, scratch);
+      if (p.pre_cta && blockIdx.x == 0 && warp >= 1) k1_delete_pre(p, H, scratch);
     }
   }
   if (tid == 0) {
@@ -1048,7 +1088,8 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
               const long long ld = p.ld;
 #pragma unroll
               for (int j = 0; j < KMAX; ++j) {
-                if (j < k) {   // (q[j] for j >= k is never read)
+                if (!GUARD) q[j] = 0.0;   // unguarded dots below: columns past k contribute exact zeros
+                if (j < k) {
                   const double qn = *sp;
                   const double2 a = H.rot[2 * j], b = H.rot[2 * j + 1];
                   const double out = fma(a.x, carry, a.y * qn);
@@ -1066,17 +1107,30 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
               if (k >= 1) qlast = S[(size_t)(k - 1) * TR + r] * H.sc[k - 1];
             }
             p.Q[(size_t)k * p.ld + grow] = df;   // unnormalised new column (lazy scale)
-            // Alg. 3-6 pass 1 (Q^T Delta f, Q^T f_i and Q_{0:k-2}^T q_{k-1}) and the norms
+            // Alg. 3-6 pass 1 (Q^T Delta f, Q^T f_i and Q_{0:k-2}^T q_{k-1}) and the norms (the
+            // words j >= k, j >= k-1 for the third, are never published)
+            if constexpr (GUARD) {
 #pragma unroll
-            for (int j = 0; j < KMAX; ++j)
-              if (j < k) {
+              for (int j = 0; j < KMAX; ++j)
+                if (j < k) {
+                  fa0[j] = fma(q[j], df, fa0[j]);
+                  fa1[j] = fma(q[j], f, fa1[j]);
+                }
+              if (xrhs) {
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j)
+                  if (j < k - 1) fa2[j] = fma(q[j], qlast, fa2[j]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < KMAX; ++j) {
                 fa0[j] = fma(q[j], df, fa0[j]);
                 fa1[j] = fma(q[j], f, fa1[j]);
               }
-            if (xrhs) {
+              if (xrhs) {
 #pragma unroll
-              for (int j = 0; j < KMAX; ++j)
-                if (j < k - 1) fa2[j] = fma(q[j], qlast, fa2[j]);
+                for (int j = 0; j < KMAX; ++j) fa2[j] = fma(q[j], qlast, fa2[j]);
+              }
             }
             fs_ff = fma(f, f, fs_ff);
             fs_dd = fma(df, df, fs_dd);

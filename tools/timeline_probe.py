@@ -40,6 +40,6 @@ for o, nm in ops.items():
     # effective SM clock from clock64 deltas (CTA 0 slots 0..5 are on one SM)
     dt = tl[o, 5] - tl[o, 0]; dc = ck[o, 5] - ck[o, 0]
     if dt > 0: print(f"         SM clock over entry..partials: {dc / dt * 1e3:.0f} MHz ({dc} cycles)")
-if det:
-    print("K4 commit detail (0 R/T stores done, 1 scale/gamma stores done, 2 Rdel stores done, 3 cs/sn done):",
-          " ".join(f"[{i}]={(t - t0) / 1e3:.2f}us/{c - int(ck[6, 1])}cyc" for i, t, c in det))
+print("K4 commit CTA: [8] warp 0 R column formed, [12..14] its QRDelete (split: early rotations loaded,"
+      " last columns rotated, last rotations), [9] done; [10] warp 1 gamma, [11] scales written;"
+      " [15] warps 3-7 R, T (and early R') written")
