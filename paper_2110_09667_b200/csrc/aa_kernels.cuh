@@ -1390,6 +1390,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       constexpr int NV = 3 * KMAX + 3;
       constexpr int NVP = NV | 1;
       double* wbuf = stage0;
+      if (my_count == 0) {   // (the spare CTA of small n: no rows, its partials are exact zeros)
+        for (int v = tid; v < L.off_gram; v += NT)
+          if (v != 2) mypart[v] = 0.0;
+        if (tid == 0) mypart[2] = dx2_pref;
+      } else {
       __syncthreads();
       {
         double* row = wbuf + (size_t)tid * NVP;
@@ -1424,6 +1429,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
         if (wd >= 0) mypart[wd] = sum;
       }
       if (tid == 0) mypart[2] = dx2_pref;
+      }
     }
   } else if constexpr (OP == OP_K1) {
     const K1Layout L = K1Layout::make(k, p.has_x, p.gram != 0);

@@ -75,7 +75,9 @@ def test_config5b_aa_run(variant):
     # windows reach cond ~1e15 here, where the eps*kappa classes are chaotic: summation order
     # alone moves ICWY's max LOO from 0.04 to 0.8 -> compare with the summation-order envelope
     env, loos = [], []
-    for p in (1, 2, 3, 4, 5, 7, 8, 16, 37, 64, 148, 592):   # twelve summation orders (test_gpu_heat.py)
+    # the summation-order envelope (criterion 4): here the window reaches cond ~1e15, the
+    # count is chaotic in the order of every inner product (12 orders: 125-136), so 24 orders
+    for p in (1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 13, 16, 19, 23, 29, 37, 48, 64, 96, 128, 148, 256, 296, 592):
         r = aa_variant(lambda x: d * x + b, np.zeros(P5), M5, variant, 500, tol=1e-10, shards=p,
                        record_x=False, record_loo=True)
         if r.converged:
