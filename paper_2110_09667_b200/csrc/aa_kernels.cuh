@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   HeadArea& H = *reinterpret_cast<HeadArea*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + head_bytes());
   double* stage0 = reinterpret_cast<double*>(smem_raw + head_bytes() + bar_bytes());
-  double* scratch = stage0;
+  double* scratch = stage0 + p.scr_off;   // aliases the stage ring unless the host separated it
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // programmatic dependent launch: this grid may be resident before its predecessor on the
@@ -902,6 +902,35 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 
   K4Head hd{};
   if (blockIdx.x == 0) AA_TL(0);
+  // tile CTAs: all, or (K4 / K1 pre_cta) all but CTA 0, which only does the factor precompute
+  const int pre = (OP == OP_K4 || OP == OP_K1) ? p.pre_cta : 0;
+  long long tb = (long long)blockIdx.x - pre, tg = (long long)gridDim.x - pre;
+  long long my_count = (tb >= 0 && ntiles > tb) ? (ntiles - 1 - tb) / tg + 1 : 0;
+  if (p.det_tpc > 0) {   // deterministic mode: CTA b streams chunk b's tiles in order
+    tb = (long long)blockIdx.x * p.det_tpc;
+    tg = 1;
+    my_count = (ntiles > tb) ? min((long long)p.det_tpc, ntiles - tb) : 0;
+  }
+  // the first tiles' TMA loads go out BEFORE the heads when the heads do not use the stage
+  // memory (their latency then overlaps the serial K3 work; at small n the head is a large
+  // share of a kernel): every op except K4 / K2 ICWY, and those two when the host gave their
+  // scratch its own region (p.scr_off > 0)
+  const bool early_tma = !(OP == OP_K4 || OP == OP_K2_ICWY) || p.scr_off > 0;
+  if (early_tma) {
+    if (tid == 0) {
+      for (int s = 0; s < NS; ++s) mbar_init(&bars[s], NWARP);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (lane == 0) {
+      fence_proxy_async();
+      for (int s = 0; s < NS && s < my_count; ++s) {
+        const long long t = tb + (long long)s * tg;
+        const long long r0 = rbeg + t * TR;
+        issue_tile_part(p, stage0 + s * stage_words, &bars[s], r0, (int)min((long long)TR, n - r0), warp);
+      }
+    }
+  }
   if constexpr (OP == OP_K4 || OP == OP_K2_ICWY) {
     if (OP == OP_K4 && tid == 0) {
       H.gdone = 0;
@@ -966,23 +995,13 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       if (p.pre_cta && blockIdx.x == 0 && warp >= 1) k1_delete_pre(p, H, scratch);
     }
   }
-  if (tid == 0) {
+  if (!early_tma && tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], NWARP);
     fence_mbar_init();
   }
-  __syncthreads();
+  __syncthreads();   // the heads' shared-memory results are complete
   if (blockIdx.x == 0) AA_TL(2);
-
-  // tile CTAs: all, or (K4 pre_cta) all but CTA 0, which only did the factor precompute
-  const int pre = (OP == OP_K4 || OP == OP_K1) ? p.pre_cta : 0;
-  long long tb = (long long)blockIdx.x - pre, tg = (long long)gridDim.x - pre;
-  long long my_count = (tb >= 0 && ntiles > tb) ? (ntiles - 1 - tb) / tg + 1 : 0;
-  if (p.det_tpc > 0) {   // deterministic mode: CTA b streams chunk b's tiles in order
-    tb = (long long)blockIdx.x * p.det_tpc;
-    tg = 1;
-    my_count = (ntiles > tb) ? min((long long)p.det_tpc, ntiles - tb) : 0;
-  }
-  if (lane == 0) {
+  if (!early_tma && lane == 0) {
     fence_proxy_async();
     for (int s = 0; s < NS && s < my_count; ++s) {
       const long long t = tb + (long long)s * tg;

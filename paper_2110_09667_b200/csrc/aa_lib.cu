@@ -350,7 +350,18 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   const size_t stage_bytes = (size_t)stages * align_up((size_t)nin * tr, 16) * sizeof(double);
   size_t scr = (OP == OP_K4) ? scratch_bytes_k4(p.m, p.variant == V_ICWY && p.icwy_merged == 2) : scratch_bytes();
   if (OP == OP_K1 && G == 0 && NCW >= 2 && NCW <= 3) scr = std::max(scr, fused_k1_table_bytes(NCW));
-  const size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
+  // the head scratch gets its own region after the stages when that fits without costing
+  // occupancy (then the first TMA loads can be issued before the heads run)
+  size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
+  p.scr_off = 0;
+  if (OP == OP_K4 || OP == OP_K2_ICWY) {
+    const size_t sep = head_bytes() + bar_bytes() + stage_bytes + scr;
+    constexpr size_t kMaxSmem = 227 * 1024, kTwoPerSm = 110 * 1024;
+    if (sep <= kMaxSmem && (smem > kTwoPerSm || sep <= kTwoPerSm)) {
+      p.scr_off = (long long)(stage_bytes / sizeof(double));
+      smem = sep;
+    }
+  }
   // per-device state of this instance (function attributes are set per device)
   constexpr int kMaxDev = 16;
   const int dev = (c->device >= 0 && c->device < kMaxDev) ? c->device : 0;
