@@ -450,12 +450,16 @@ def main():
         s.init(x, Gn(x), xn)
         x, xn = xn, x
         gs = [torch.empty_like(x) for _ in range(2)]
+        # b is nudged every step (outside the timed bracket), so the small problem never
+        # reaches its fixed point exactly: Delta f = 0 would be a breakdown (reading A12)
         for i in range(m + warmup):
+            bn.mul_(1.0 + 1e-3)
             s.step(x, torch.addcmul(bn, dn, x, out=gs[i % 2]), xn)
             x, xn = xn, x
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         barrier()
         for i in range(steps):
+            bn.mul_(1.0 + 1e-3)
             g = torch.addcmul(bn, dn, x, out=gs[i % 2])
             ev[i][0].record(stream)
             s.step(x, g, xn)

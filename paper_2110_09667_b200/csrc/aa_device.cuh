@@ -164,6 +164,7 @@ struct alignas(64) KParams {
   int* bd_host;     // device alias of the handle's mapped pinned breakdown word (polled by aa_step)
   int det_tpc;      // deterministic mode: tiles per DET_ROWS chunk (CTA b = chunk b); 0 = off
   long long scr_off; // head scratch at stage0 + scr_off doubles (0: aliases the stage ring)
+  int early_tma;    // the first tiles' loads may be issued before the heads (AA_NO_EARLY_TMA=1: off)
 };
 
 // ------------------------------------------------------------------ PTX wrappers

@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   // memory (their latency then overlaps the serial K3 work; at small n the head is a large
   // share of a kernel): every op except K4 / K2 ICWY, and those two when the host gave their
   // scratch its own region (p.scr_off > 0)
-  const bool early_tma = !(OP == OP_K4 || OP == OP_K2_ICWY) || p.scr_off > 0;
+  const bool early_tma = p.early_tma && (!(OP == OP_K4 || OP == OP_K2_ICWY) || p.scr_off > 0);
   if (early_tma) {
     if (tid == 0) {
       for (int s = 0; s < NS; ++s) mbar_init(&bars[s], NWARP);
@@ -1550,13 +1550,33 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       if (lane == 0) outv[w] = sum;
     }
   } else
-  for (int w = tid; w < p.words; w += NT) {
-    double s = 0.0;
-#pragma unroll 4
-    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(p.part + (size_t)b * LRED + w);   // CTA order
-    // row-chunked launches (aa_step_host) add to the previous chunks' sums, in chunk order
-    if (!p.chunk_first) s += (OP == OP_K4) ? (w == 0 ? p.st->dx2_acc : 0.0) : outv[w];
-    outv[w] = s;
+  {
+    // K lanes per word (a power of two: as many as the words leave, at most a warp): lane q of a
+    // word's group sums the CTAs b = q, q + K, ... in order (independent loads in flight), then
+    // a fixed butterfly across the group -- a fixed order for a given grid, so results stay
+    // bitwise reproducible; one thread walking all CTAs serially costs a full L2 latency per
+    // few CTAs (296 CTAs at n >= 1.5e6: ~20 us per launch)
+    const int words = p.words;
+    const int G = (int)gridDim.x;
+    int K = 32;
+    while (K > 1 && K * words > NT) K >>= 1;
+    const int q = tid & (K - 1), grp = tid / K, ngrp = NT / K;
+    const int rounds = (words + ngrp - 1) / ngrp;
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int w = grp + rd * ngrp;
+      const bool valid = w < words;
+      double s = 0.0;
+      if (valid) {
+#pragma unroll 8
+        for (int b = q; b < G; b += K) s += __ldcg(p.part + (size_t)b * LRED + w);
+      }
+      for (int o = K >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (valid && q == 0) {
+        // row-chunked launches (aa_step_host) add to the previous chunks' sums, in chunk order
+        if (!p.chunk_first) s += (OP == OP_K4) ? (w == 0 ? p.st->dx2_acc : 0.0) : outv[w];
+        outv[w] = s;
+      }
+    }
   }
   __syncthreads();
   if constexpr (OP != OP_K4) {

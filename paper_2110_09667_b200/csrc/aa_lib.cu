@@ -353,8 +353,10 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   // the head scratch gets its own region after the stages when that fits without costing
   // occupancy (then the first TMA loads can be issued before the heads run)
   size_t smem = head_bytes() + bar_bytes() + std::max(stage_bytes, scr);
+  static const bool early_off = getenv("AA_NO_EARLY_TMA") && atoi(getenv("AA_NO_EARLY_TMA")) != 0;
+  p.early_tma = early_off ? 0 : 1;
   p.scr_off = 0;
-  if (OP == OP_K4 || OP == OP_K2_ICWY) {
+  if ((OP == OP_K4 || OP == OP_K2_ICWY) && !early_off) {
     const size_t sep = head_bytes() + bar_bytes() + stage_bytes + scr;
     constexpr size_t kMaxSmem = 227 * 1024, kTwoPerSm = 110 * 1024;
     if (sep <= kMaxSmem && (smem > kTwoPerSm || sep <= kTwoPerSm)) {
@@ -403,6 +405,10 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   if (OP == OP_K4 && !c->det && ntiles >= 1 && ntiles + 1 <= (long long)c->sms * per_sm) {
     p.pre_cta = 1;
     grid = ntiles + 1;
+  } else if (OP == OP_K4 && !c->det && ntiles <= 32 * (long long)c->sms * per_sm && grid >= 2) {
+    // mid n: CTA 0 still only commits (its ~3 us of serial head work would otherwise delay its
+    // share of the tiles, the kernel's tail); the other CTAs take every tile
+    p.pre_cta = 1;
   }
   // K1 when the tiles do not fill the GPU: one extra CTA (CTA 0) computes the early rotations of
   // the next QRDelete (k1_delete_pre) while the others stream; K4 then only finishes them
@@ -481,7 +487,11 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
   p.fp = c->fp;
   p.gp = c->gp;
   if constexpr (OP == OP_K1) {
-    const int ncw = (p.flags & F_DELETE_ONLY) ? 1 : (p.k + 2 + NWARP - 1) / NWARP;
+    int ncw = (p.flags & F_DELETE_ONLY) ? 1 : (p.k + 2 + NWARP - 1) / NWARP;
+    // AA_K1_NOFUSE=1 (A/B only): the split row pass + block multi-dot instead of the fused one
+    // (an NCW = 4 instance covers up to 30 columns, unused warps' columns are skipped)
+    static const bool nofuse = getenv("AA_K1_NOFUSE") && atoi(getenv("AA_K1_NOFUSE")) != 0;
+    if (nofuse && !gram && (ncw == 2 || ncw == 3)) ncw = 4;
     if (gram) {
       const int kg = (p.flags & F_DELETE_ONLY) ? p.c_in - 1 : p.k;
       const int nb8 = (kg + 7) / 8;
