@@ -326,14 +326,14 @@ def main():
 
     ar_mode = {"mode": "ncclAllReduce" if world > 1 else "none (1 rank)"}
 
-    def make_solver(nl, m, variant, **kw):
+    def make_solver(nl, m, variant, stream_override=None, **kw):
         # the kernel study times full recycle steps: with m = 50 (and m = 20 after the timed
         # steps) this problem's residual is at rounding level, where a new column can pass the
         # breakdown threshold (reading A12) and the step would degrade to x = G(x) (skipping
         # K4's products) -- the breakdown test is set to R_kk = 0 / NaN only (eps_a = 0)
         kw.setdefault("breakdown_eps", 0.0)
         s = aa.AndersonSolver(nl, m, variant, rank=rank, nranks=world, unique_id=uid, nccl_comm=comm,
-                              stream=stream, **kw)
+                              stream=stream_override or stream, **kw)
         if args.fused_ar and world > 1:
             try:
                 aa.aa_set_option(s.h, aa.OPT_FUSED_ALLREDUCE, 1)
@@ -473,6 +473,64 @@ def main():
                 "us_per_iter_min": max_over_ranks(t[0]) * 1e3, "allreduces": st.allreduce_last,
                 "sync_points": st.sync_points_last}
 
+    def measure_n_graph(variant, m, nl, reps=20):
+        """The same small-n step with the caller's loop captured in a CUDA graph: one period of
+        lcm(2, m) recycle steps (G included; the factor version and the Delta G ring head repeat
+        with that period, the exchange sequence numbers come from a device counter), replayed.
+        Returns us per AA step with G subtracted (G's own graph timed alone)."""
+        import math
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            dn = torch.empty(nl, dtype=torch.float64, device="cuda")
+            bn = torch.empty_like(dn)
+            aa.aa_fill_uniform(dn, nl, -0.9, 0.9, stream_id=1, offset=rank * nl, stream=st)
+            aa.aa_fill_uniform(bn, nl, -1.0, 1.0, stream_id=2, offset=rank * nl, stream=st)
+            base, extra = split_variant(variant)
+            s = make_solver(nl, m, base, stream_override=st, **extra)
+            x = torch.zeros(nl, dtype=torch.float64, device="cuda")
+            xn = torch.empty_like(x)
+            g = torch.empty_like(x)
+            s.init(x, torch.addcmul(bn, dn, x), xn)
+            x, xn = xn, x
+            for _ in range(m + 3):
+                bn.mul_(1.0 + 1e-3)
+                torch.addcmul(bn, dn, x, out=g)
+                s.step(x, g, xn)
+                x, xn = xn, x
+            L = m * 2 // math.gcd(m, 2)
+            bufs = (x, xn)
+
+            def window(with_aa=True):
+                for i in range(L):
+                    a, c = bufs[i % 2], bufs[(i + 1) % 2]
+                    bn.mul_(1.0 + 1e-3)
+                    torch.addcmul(bn, dn, a, out=g)
+                    if with_aa:
+                        s.step(a, g, c)
+
+            times = []
+            for with_aa in (True, False):
+                st.synchronize()
+                if dist is not None:
+                    dist.barrier()
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=st):
+                    window(with_aa)
+                gr.replay()
+                st.synchronize()
+                if dist is not None:
+                    dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(reps):
+                    gr.replay()
+                e1.record(st)
+                st.synchronize()
+                times.append(e0.elapsed_time(e1) / (reps * L) * 1e3)
+                del gr
+            s.close()
+        return {"us_per_iter_graph": max_over_ranks(times[0] - times[1]), "us_G_graph": max_over_ranks(times[1])}
+
     V = 8 * n_local
     head, clocks, e2e = measure(args.variant, args.m, args.steps, args.warmup, with_clocks=True,
                                 e2e=not args.no_e2e)
@@ -515,6 +573,8 @@ def main():
         for nl in (1000, 10000, 100000, 1500000, 10000000):
             for v in VARIANTS + EXTRA_VARIANTS:
                 small_n[f"{v}_n{nl}"] = measure_n(v, args.m, nl, 20, 5)
+                if nl <= 1500000:
+                    small_n[f"{v}_n{nl}"].update(measure_n_graph(v, args.m, nl))
 
     xlat = {}
     if world > 1 and not args.only_headline:
