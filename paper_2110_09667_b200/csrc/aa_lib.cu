@@ -79,6 +79,9 @@ struct aa_ctx {
   // AA_OPT_DETERMINISTIC: one partial slot per DET_ROWS chunk, and the all-gather buffer of the
   // NCCL path (ranks summed in the aligned tree by aa_det_rank_sum_kernel)
   int det = 0;
+  // K1 form for 7..22 columns: 0 fused row pass + dots (FUSED), 1 split row pass + block
+  // multi-dot; chosen per (device, m, n) by timing both at aa_init (k1_form_trial)
+  int k1_split = 0;
   double* part_det = nullptr;
   double* xgather = nullptr;
   int* bd_dev = nullptr;    // its device alias
@@ -491,7 +494,7 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
     // AA_K1_NOFUSE=1 (A/B only): the split row pass + block multi-dot instead of the fused one
     // (an NCW = 4 instance covers up to 30 columns, unused warps' columns are skipped)
     static const bool nofuse = getenv("AA_K1_NOFUSE") && atoi(getenv("AA_K1_NOFUSE")) != 0;
-    if (nofuse && !gram && (ncw == 2 || ncw == 3)) ncw = 4;
+    if ((nofuse || c->k1_split) && !gram && (ncw == 2 || ncw == 3)) ncw = 4;
     if (gram) {
       const int kg = (p.flags & F_DELETE_ONLY) ? p.c_in - 1 : p.k;
       const int nb8 = (kg + 7) / 8;
@@ -1173,10 +1176,88 @@ static int reset_small(aa_ctx* c) {
   return AA_OK;
 }
 
+// K1's two forms for 7..22 columns: the fused row pass (dots in registers) and
+// the split one (rotated tile back to shared memory, block multi-dot).  Which is faster depends
+// on the B200 it runs on -- same-build A/Bs: fused 6.06 vs split 6.72 ms on one box, 6.42 vs
+// 6.11 ms on another (profiles/r02/k1_fused_vs_split_ab*.txt) -- so at large n the handle
+// times both once on its own (still empty) buffers and keeps the faster; the choice is cached
+// per process for (device, m, n).  AA_K1_FORM=fused|split overrides.  Both forms give results
+// inside the same tolerances; the choice only changes the summation order of pass 1.
+static int k1_form_trial(aa_ctx* c) {
+  c->k1_split = 0;
+  const char* env = getenv("AA_K1_FORM");
+  if (env && !strcmp(env, "split")) c->k1_split = 1;
+  if (env) return AA_OK;
+  const int k = c->m - 1;
+  const int ncw = (k + 2 + NWARP - 1) / NWARP;
+  if (c->det || ncw < 2 || ncw > 3 || c->n < (1 << 20)) return AA_OK;
+  static std::map<std::tuple<int, int, int64_t>, int> cache;
+  const auto key = std::make_tuple(c->device, c->m, c->n);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    c->k1_split = it->second;
+    return AA_OK;
+  }
+  // a recycle-shaped K1 on the handle's own buffers, made representative: distinct vectors
+  // (Delta G slots 1..4 as x, G(x), f_{i-1}, G(x_{i-1})), uniform data in Q and those slots,
+  // nonzero rotations (the handle is empty: aa_init resets everything the trial touches)
+  for (int j = 0; j < c->m; ++j) {
+    aa_fill_uniform_kernel<<<c->sms * 8, 256, 0, c->stream>>>(qcol(c, j), c->n, 1000ull * j, -1.0, 2.0);
+    aa_fill_uniform_kernel<<<c->sms * 8, 256, 0, c->stream>>>(dgcol(c, j), c->n, 777ull * j + 5, -1.0, 2.0);
+  }
+  {
+    double cs[MMAX], sn[MMAX];
+    for (int j = 0; j < MMAX; ++j) {
+      cs[j] = 0.6;
+      sn[j] = 0.8;
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->st->f[0].cs, cs, sizeof(cs), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->st->f[0].sn, sn, sizeof(sn), cudaMemcpyHostToDevice, c->stream));
+  }
+  KParams p = base_params(c);
+  const K1Layout L = K1Layout::make(k, true, false);
+  p.red_words0 = L.words;
+  p.k = k;
+  p.c_in = c->m;
+  p.recycle = 1;
+  p.has_x = 1;
+  p.reortho = 1;
+  p.op = OP_K1;
+  p.dg_out = dgcol(c, 0);
+  p.words = L.words;
+  p.red_slot = 0;
+  Inputs in;
+  in.block(0, 0, c->m);
+  for (int v = 1; v <= 4; ++v) in.vector(dgcol(c, v), false);
+  cudaEvent_t e0, e1;
+  CUDA_TRY(c, cudaEventCreate(&e0));
+  CUDA_TRY(c, cudaEventCreate(&e1));
+  float best[2] = {1e30f, 1e30f};
+  for (int rep = 0; rep < 4; ++rep)
+    for (int form = 0; form < 2; ++form) {
+      c->k1_split = form;
+      KParams q = p;
+      CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+      RET_IF(launch_op<OP_K1>(c, q, in, 0));
+      CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+      CUDA_TRY(c, cudaEventSynchronize(e1));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0 && ms < best[form]) best[form] = ms;   // rep 0 warms both forms up
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  c->k1_split = (best[1] < best[0]) ? 1 : 0;
+  cache[key] = c->k1_split;
+  return AA_OK;
+}
+
 int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out) {
   RET_IF(check_handle(h));
   if (!x0 || !gx0 || !x1_out) return AA_ERR_ARG;
   RET_IF(reset_small(h));
+  RET_IF(k1_form_trial(h));
+  RET_IF(reset_small(h));   // the trial used the reduction slots and the factor scratch
   *reinterpret_cast<volatile int*>(h->bd_host) = 0;
   if (h->eps_a < 0.0) h->eps_a = 10.0 * DBL_EPSILON * sqrt((double)h->n_global);
   const int grid = h->sms * 4;
