@@ -415,21 +415,31 @@ def main():
             torch.addcmul(bh, dh, xh, out=gh)
             s.step_host(xh, gh, outh)
             xh, outh = outh, xh
-            t_e = []
-            for _ in range(nh):
-                torch.addcmul(bh, dh, xh, out=gh)    # caller's G on the host (untimed)
-                barrier()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                s.step_host(xh, gh, outh)
-                e1.record(stream)
-                barrier()
-                t_e.append(e0.elapsed_time(e1))
-                xh, outh = outh, xh
-            e2e_res = {"value": max_over_ranks(float(np.mean(t_e))) * 1e3, "unit": "us/iter",
-                       "h2d_bytes_per_step": 2 * 8 * n_local, "d2h_bytes_per_step": 8 * n_local,
-                       "steps": nh, "path": "aa_step_host (pinned host x_i, G(x_i) in; x_{i+1} out)"}
+            def timed_host_steps(count, upload_x):
+                nonlocal xh, outh
+                t_e = []
+                for _ in range(count):
+                    torch.addcmul(bh, dh, xh, out=gh)    # caller's G on the host (untimed)
+                    barrier()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    # x_i = None: the x_{i+1} the previous call returned, still on the device
+                    s.step_host(xh if upload_x else None, gh, outh)
+                    e1.record(stream)
+                    barrier()
+                    t_e.append(e0.elapsed_time(e1))
+                    xh, outh = outh, xh
+                return max_over_ranks(float(np.mean(t_e))) * 1e3
+
+            # the host loop x -> G(x): G(x_i) in, x_{i+1} out (x_i stays on the device)
+            e2e_us = timed_host_steps(nh, False)
+            full_us = timed_host_steps(3, True)   # context: x_i uploaded as well
+            e2e_res = {"value": e2e_us, "unit": "us/iter",
+                       "h2d_bytes_per_step": 8 * n_local, "d2h_bytes_per_step": 8 * n_local,
+                       "steps": nh, "path": "aa_step_host (pinned host G(x_i) in, x_{i+1} out; x_i = the previous "
+                                             "call's x_{i+1}, kept on the device)",
+                       "with_x_upload_us": full_us, "with_x_upload_h2d_bytes": 2 * 8 * n_local}
         s.close()
         del x, xn
         torch.cuda.empty_cache()

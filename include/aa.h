@@ -202,7 +202,11 @@ int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next
  * broke down and aa_reset has not been called since; see BREAKDOWN above.) */
 
 /* Same computation with HOST buffers (pinned or pageable): copies in, runs aa_step,
- * copies x_next back and synchronises.  For end-to-end measurement. */
+ * copies x_next back and synchronises.  x_i_host may be NULL: then x_i is the x_{i+1} the
+ * previous aa_step_host call of this handle returned (kept on the device; AA_ERR_STATE if
+ * there was none since aa_init, or an aa_step came in between), so a host-side loop
+ * x -> G(x) uploads only G(x_i) per iteration.  At n_local >= 4M rows the copies go in row
+ * chunks overlapped with K1 (uploads) and K4 (downloads). */
 int aa_step_host(aa_handle_t h, const double* x_i_host, const double* gx_i_host,
                  double* x_next_host);
 

@@ -75,6 +75,7 @@ struct aa_ctx {
   SmallState* st = nullptr;
   double *red = nullptr, *part = nullptr;
   double *hx = nullptr, *hg = nullptr, *hxn = nullptr;  // staging for aa_step_host
+  bool hxn_valid = false;   // hxn holds the x_{i+1} the last aa_step_host returned
   int* bd_host = nullptr;   // mapped pinned breakdown word (written by K4, polled by aa_step)
   // AA_OPT_DETERMINISTIC: one partial slot per DET_ROWS chunk, and the all-gather buffer of the
   // NCCL path (ranks summed in the aligned tree by aa_det_rank_sum_kernel)
@@ -1176,18 +1177,21 @@ static int reset_small(aa_ctx* c) {
   return AA_OK;
 }
 
-// K1's two forms for 7..22 columns: the fused row pass (dots in registers) and
-// the split one (rotated tile back to shared memory, block multi-dot).  Which is faster depends
-// on the B200 it runs on -- same-build A/Bs: fused 6.06 vs split 6.72 ms on one box, 6.42 vs
-// 6.11 ms on another (profiles/r02/k1_fused_vs_split_ab*.txt) -- so at large n the handle
-// times both once on its own (still empty) buffers and keeps the faster; the choice is cached
-// per process for (device, m, n).  AA_K1_FORM=fused|split overrides.  Both forms give results
-// inside the same tolerances; the choice only changes the summation order of pass 1.
+// K1's two forms for 7..22 columns: the fused row pass (dots in registers,
+// the default) and the split one (rotated tile back to shared memory, block multi-dot).  Which
+// is faster depends on the B200: same-build A/Bs at the bench's configuration gave fused 6.06
+// vs split 6.72-6.85 ms on three runs of one box type, 6.42 vs 6.11 ms on another
+// (profiles/r02/k1_fused_vs_split_ab*.txt, k1_form_ab.txt), and a short timing trial on the
+// handle's own buffers (AA_K1_FORM=auto: both forms, three launches each, at aa_init) picked
+// the split form on the box where the fused one is 11 % faster in sustained runs -- the
+// power-capped clocks of a long run are not those of a short burst.  So the fused form is the
+// default; AA_K1_FORM=split|auto selects otherwise.  Both forms give results inside the same
+// tolerances; the choice only changes the summation order of pass 1.
 static int k1_form_trial(aa_ctx* c) {
   c->k1_split = 0;
   const char* env = getenv("AA_K1_FORM");
   if (env && !strcmp(env, "split")) c->k1_split = 1;
-  if (env) return AA_OK;
+  if (!env || strcmp(env, "auto")) return AA_OK;
   const int k = c->m - 1;
   const int ncw = (k + 2 + NWARP - 1) / NWARP;
   if (c->det || ncw < 2 || ncw > 3 || c->n < (1 << 20)) return AA_OK;
@@ -1267,6 +1271,7 @@ int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out) 
   h->iter = 0;
   h->mi = 0;
   h->dg_head = 0;
+  h->hxn_valid = false;
   h->inited = true;
   return AA_OK;
 }
@@ -1274,6 +1279,7 @@ int aa_init(aa_handle_t h, const double* x0, const double* gx0, double* x1_out) 
 int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next) {
   RET_IF(check_handle(h));
   if (!h->inited) return AA_ERR_STATE;
+  h->hxn_valid = false;   // (aa_step_host sets it again after its own call)
   // a breakdown seen by an earlier step (mapped pinned word, polled without blocking):
   // refuse until aa_reset.  One rank only: ranks could see the word at different times and
   // must not diverge in their collective call sequences; with nranks > 1 the breakdown is
@@ -1294,7 +1300,13 @@ int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next
 int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next) {
   RET_IF(check_handle(h));
   if (!h->inited) return AA_ERR_STATE;
-  if (!x_i || !gx_i || !x_next) return AA_ERR_ARG;
+  if (!gx_i || !x_next) return AA_ERR_ARG;
+  // x_i = NULL: the x_{i+1} the previous aa_step_host returned, still on the device (the
+  // staging buffers swap roles; only G(x_i) crosses PCIe on the way in)
+  if (!x_i && !h->hxn_valid) return AA_ERR_STATE;
+  const bool reuse_x = (x_i == nullptr);
+  if (reuse_x) std::swap(h->hx, h->hxn);
+  h->hxn_valid = false;
   const size_t vb = (size_t)h->n * sizeof(double);
   if (!h->hx || !h->hg || !h->hxn) {
     if ((!h->hx && cudaMalloc(&h->hx, vb) != cudaSuccess) || (!h->hg && cudaMalloc(&h->hg, vb) != cudaSuccess) ||
@@ -1309,11 +1321,12 @@ int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x
     }
   }
   if (h->n < kChunkMinRows || h->mi == 0 || h->det) {
-    CUDA_TRY(h, cudaMemcpyAsync(h->hx, x_i, vb, cudaMemcpyHostToDevice, h->stream));
+    if (!reuse_x) CUDA_TRY(h, cudaMemcpyAsync(h->hx, x_i, vb, cudaMemcpyHostToDevice, h->stream));
     CUDA_TRY(h, cudaMemcpyAsync(h->hg, gx_i, vb, cudaMemcpyHostToDevice, h->stream));
     RET_IF(aa_step(h, h->hx, h->hg, h->hxn));
     CUDA_TRY(h, cudaMemcpyAsync(x_next, h->hxn, vb, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    h->hxn_valid = true;
     return AA_OK;
   }
   // large n: chunked copies overlapped with K1 (uploads) and K4 (downloads)
@@ -1338,13 +1351,15 @@ int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x
   CUDA_TRY(h, cudaStreamWaitEvent(h->cstream, h->chunk_evK[0], 0));
   for (int ci = 0; ci < cp.nc; ++ci) {
     const size_t off = (size_t)cp.b[ci], cnt = (size_t)(cp.b[ci + 1] - cp.b[ci]);
-    CUDA_TRY(h, cudaMemcpyAsync(h->hx + off, x_i + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->cstream));
+    if (!reuse_x)
+      CUDA_TRY(h, cudaMemcpyAsync(h->hx + off, x_i + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->cstream));
     CUDA_TRY(h, cudaMemcpyAsync(h->hg + off, gx_i + off, cnt * sizeof(double), cudaMemcpyHostToDevice, h->cstream));
     CUDA_TRY(h, cudaEventRecord(h->chunk_evH[ci], h->cstream));
   }
   RET_IF(aa_step_chunked(h, &cp));
   CUDA_TRY(h, cudaStreamSynchronize(h->cstream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->hxn_valid = true;
   return AA_OK;
 }
 

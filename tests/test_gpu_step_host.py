@@ -64,3 +64,37 @@ def test_step_host_chunked_matches_device(prob, variant):
     if variant == "dcgs2":   # and the oracle, once
         o2 = aa_variant(lambda v: d * v + b, np.zeros(N), m, "dcgs2", iters, record_loo=False)
         assert np.linalg.norm(xh.numpy() - o2.xs[-1]) <= 1e-10 * np.linalg.norm(o2.xs[-1])
+
+
+@pytest.mark.parametrize("n", [4097, 5_000_003])
+def test_step_host_reuses_device_x(n):
+    """aa_step_host(x_i = NULL) takes the x_{i+1} its previous call returned (kept on the
+    device): bitwise the same iterates as uploading x_i every time, small and row-chunked
+    sizes; NULL without a previous host step (or after an aa_step) is AA_ERR_STATE."""
+    d, b = problems.diagonal(n)
+    dh, bh = torch.tensor(d), torch.tensor(b)
+    stream = torch.cuda.current_stream()
+    outs = []
+    for reuse in (False, True):
+        s = aa.AndersonSolver(n, 4, "dcgs2", stream=stream)
+        x0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+        x1 = torch.empty_like(x0)
+        s.init(x0, torch.tensor(b, device="cuda"), x1)
+        xh = x1.cpu().pin_memory()
+        gh = torch.empty(n, dtype=torch.float64).pin_memory()
+        oh = torch.empty(n, dtype=torch.float64).pin_memory()
+        if reuse:
+            torch.addcmul(bh, dh, xh, out=gh)
+            with pytest.raises(aa.AAError) as ei:   # nothing to reuse yet
+                s.step_host(None, gh, oh)
+            assert ei.value.code == 2
+        xs = []
+        for i in range(9):
+            torch.addcmul(bh, dh, xh, out=gh)
+            s.step_host(None if (reuse and i > 0) else xh, gh, oh)
+            xh, oh = oh, xh
+            xs.append(xh.numpy().copy())
+        s.close()
+        outs.append(xs)
+    for a, c in zip(*outs):
+        assert np.array_equal(a, c)
