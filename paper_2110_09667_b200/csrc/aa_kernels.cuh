@@ -691,10 +691,12 @@ __device__ __forceinline__ int gram_block_I(int blk) {
 // stage ring is idle after the tile loop), in chunks of blocks, and write this CTA's
 // partial words.  mode 0: strict lower, rows < kg-1 -> off_gram, row kg-1 -> off_x (ICWY
 // after QRDelete + Alg. 4 l.1); 1: strict lower packed (stand-alone delete); 2: lower incl.
-// diagonal packed (loss of orthogonality).
+// diagonal packed (loss of orthogonality); 3: mode 0 over the kg-2 columns of Q, then row
+// kg-2 (Delta f) -> off_df and df.df, row kg-1 (f_i) -> off_f, df.f and f.f (K1 words 1, 3, 0).
 template <int NB8>
 __device__ void gram_epilogue(const KParams& p, const double* gc0, const double* gc1, double* buf,
-                              double* mypart, int kg, int mode, int off_x, int off_gram) {
+                              double* mypart, int kg, int mode, int off_x, int off_gram, int off_df,
+                              int off_f) {
   constexpr int GB = NB8 * (NB8 + 1) / 2;
   constexpr int CH = 8;  // blocks per chunk: 8 warps x 8 blocks x 64 doubles = 32 KB
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -717,7 +719,19 @@ __device__ void gram_epilogue(const KParams& p, const double* gc0, const double*
       const int ln = w >> 1, ee = w & 1;
       const int i = 8 * I + (ln >> 2), j = 8 * J + 2 * (ln & 3) + ee;
       if (i >= kg) continue;
-      if (mode == 2) {
+      if (mode == 3) {
+        const int kq = kg - 2;
+        if (j > i) continue;
+        int wd = -1;
+        if (i < kq) {
+          if (j < i) wd = (i == kq - 1) ? off_x + j : off_gram + i * (i - 1) / 2 + j;
+        } else if (i == kq) {
+          wd = (j < kq) ? off_df + j : 1;
+        } else {
+          wd = (j < kq) ? off_f + j : (j == kq ? 3 : 0);
+        }
+        if (wd >= 0) mypart[wd] = s;
+      } else if (mode == 2) {
         if (j <= i) mypart[i * (i + 1) / 2 + j] = s;
       } else if (j < i) {
         int wd;
@@ -868,6 +882,10 @@ __device__ void fused_exchange(const KParams& p, double* v, int cnt, unsigned lo
 template <int OP, int NCW, int NB8>
 __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant__ KParams p) {
   constexpr bool GRAM = NB8 > 0;
+  // K1 with the Gram and no block multi-dot (NCW = 0): Delta f and f_i are Gram columns k and
+  // k+1, so the one DMMA pass gives T's row, the post-delete Gram, Q^T Delta f, Q^T f_i and the
+  // three norms
+  constexpr bool GX = (OP == OP_K1) && GRAM && NCW == 0;
   // K1 without a Gram and with 7..22 columns (NCW 2..3; with fewer the split form measured
   // faster -- two CTAs per SM hide it): the block multi-dot is fused into
   // the row-wise pass -- each thread keeps its rows' products with Delta f, f_i and q_{k-1} in
@@ -1044,6 +1062,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   const bool del_only = p.flags & F_DELETE_ONLY;
   const int kg = (OP == OP_GRAM) ? p.c_in : (del_only ? p.c_in - 1 : k);
   const bool do_gram = GRAM && p.gram != 0 && (OP == OP_GRAM ? kg >= 1 : kg >= 2);
+  const int kgx = GX ? k + 2 : kg;   // Gram columns
   int gfrag[NB8 > 0 ? NB8 : 1];
   {
     const int g_r = lane >> 2, g_c = lane & 3;
@@ -1052,7 +1071,10 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
 #pragma unroll
     for (int X = 0; X < (NB8 > 0 ? NB8 : 1); ++X) {
       const int col = 8 * X + g_r;
-      gfrag[X] = (col < kg) ? col * TR + g_c : -1;   // columns past kg contribute 0
+      int slot = (col < kg) ? col : -1;   // columns past kgx contribute 0
+      if (GX && col == k) slot = H.lcol[k + 1];   // Delta f
+      if (GX && col == k + 1) slot = vb;          // f_i
+      gfrag[X] = (slot >= 0) ? slot * TR + g_c : -1;
     }
   }
 
@@ -1487,7 +1509,9 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
       if (tid == 0) mypart[2] = dx2_pref;
     }
     if constexpr (GRAM) {
-      if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, del_only ? 1 : 0, L.off_x, L.off_gram);
+      if (do_gram)
+        gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kgx, GX ? 3 : (del_only ? 1 : 0), L.off_x, L.off_gram,
+                           L.off_df, L.off_f);
     }
   } else if constexpr (OP == OP_K2A_CGS2) {
 #pragma unroll
@@ -1500,7 +1524,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     }
   } else if constexpr (OP == OP_GRAM) {
     if constexpr (GRAM) {
-      if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, 2, 0, 0);
+      if (do_gram) gram_epilogue<NB8>(p, gc0, gc1, stage0, mypart, kg, 2, 0, 0, 0, 0);
     }
   } else {
     // row-wise accumulators: block reduction

@@ -511,6 +511,21 @@ int launch_op(aa_ctx* c, KParams& p, const Inputs& in, int cls) {
           default: return launch_inst<OP_K1, 1, 8>(c, p, smem, cls);
         }
       }
+      // Delta f and f_i as Gram columns k, k+1 when they fit the k columns' 8-column blocks
+      // (k mod 8 in 1..6; AA_GRAM_MULTIDOT=1 keeps the block multi-dot, A/B only)
+      static const bool gram_md = getenv("AA_GRAM_MULTIDOT") && atoi(getenv("AA_GRAM_MULTIDOT")) != 0;
+      if (!gram_md && (p.k + 2 + 7) / 8 == nb8) {
+        switch (nb8) {
+          case 1: return launch_inst<OP_K1, 0, 1>(c, p, smem, cls);
+          case 2: return launch_inst<OP_K1, 0, 2>(c, p, smem, cls);
+          case 3: return launch_inst<OP_K1, 0, 3>(c, p, smem, cls);
+          case 4: return launch_inst<OP_K1, 0, 4>(c, p, smem, cls);
+          case 5: return launch_inst<OP_K1, 0, 5>(c, p, smem, cls);
+          case 6: return launch_inst<OP_K1, 0, 6>(c, p, smem, cls);
+          case 7: return launch_inst<OP_K1, 0, 7>(c, p, smem, cls);
+          default: return launch_inst<OP_K1, 0, 8>(c, p, smem, cls);
+        }
+      }
       switch (nb8) {
         AA_K1_GRAM_CASE(1)
         AA_K1_GRAM_CASE(2)
