@@ -1549,15 +1549,15 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   if (blockIdx.x == 0) AA_TL(5);
   // ------------------------------------------------------------ cross-CTA reduction
   if (gridDim.x > 1) {
-    // the barrier orders every thread's partial stores before thread 0's GPU-scope fence
-    // (fences are cumulative), which publishes them with the ticket; the last CTA's thread 0
-    // fences again (acquire side) before its CTA reads the partials through L2 (__ldcg)
+    // the barrier orders every thread's partial stores before thread 0's ticket, an
+    // acquire-release atomic at GPU scope: its release half publishes them (cumulatively),
+    // its acquire half orders the last CTA's reads of the others' partials (through L2,
+    // __ldcg, after the next barrier) -- no separate fences
     __syncthreads();
     if (tid == 0) {
-      __threadfence();
-      const unsigned int t = atomicAdd(&p.st->counter, 1u);
+      unsigned int t;
+      asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(&p.st->counter) : "memory");
       H.is_last = (t == gridDim.x - 1);
-      if (H.is_last) __threadfence();
     }
     __syncthreads();
     if (!H.is_last) return;
