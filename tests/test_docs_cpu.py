@@ -26,7 +26,7 @@ def test_cited_evidence_files_exist():
             if "*" in name or name in ("SPEC.md", "PAPER.md"):   # the reference's own documents
                 continue
             for n in _expand(name):
-                dirs = ("", base, "profiles", "profiles/r01", "profiles/r01/history", "profiles/r02", "tools", "tests",
+                dirs = ("", base, "profiles", "profiles/r01", "profiles/r01/history", "profiles/r02", "profiles/r02final", "tools", "tests",
                         "include", "oracle", "aa_inputs", "paper_2110_09667_b200", "paper_2110_09667_b200/csrc")
                 candidates = [os.path.join(ROOT, d, n) for d in dirs]
                 if not any(os.path.exists(c) for c in candidates):
