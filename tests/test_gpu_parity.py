@@ -116,6 +116,29 @@ def test_ragged_sizes_and_windows(n, m, variant):
         assert np.isfinite(a).all()
 
 
+@pytest.mark.parametrize("m", [3, 8, 9, 17, 34, 41, 58, 64])
+def test_icwy_gram_column_forms(m):
+    """ICWY's recycle K1 carries the Gram in two forms: Delta f and f_i as
+    Gram columns k, k+1 when they fit the k columns' 8-column groups (k mod 8 in 1..6:
+    m = 3, 34, 58) and the block multi-dot beside the Gram otherwise (k mod 8 in {0, 7}:
+    m = 8, 9, 17, 41, 64); both against O2 through start-up and 8 recycle steps."""
+    n = 20003
+    # spectrum in [-0.5, 0.99): slow enough that m = 64 reaches recycle unconverged, and the
+    # oracle's own iterates agree to ~1e-14 across summation orders (row permutations); on
+    # [0.5, 0.99) they spread to 1e-10..1e-3, so no implementation could be held to 1e-10 there
+    d, b = problems.diagonal(n, -0.5, 0.99)
+    dt, bt = torch.tensor(d, device="cuda"), torch.tensor(b, device="cuda")
+    iters = m + 9
+    o2 = aa_variant(lambda x: d * x + b, np.zeros(n), m, "icwy", iters, breakdown="restart")
+    gpu = run_gpu(lambda x: dt * x + bt, np.zeros(n), m, "icwy", iters)
+    K = next((i for i, f in enumerate(o2.f_norms) if f < 1e-11 * np.linalg.norm(o2.x1)), iters)
+    assert K > m + 1, K   # the comparison reaches recycle steps
+    assert _rel_x(gpu, o2, K) <= 1e-10
+    for i in range(K):
+        assert gpu.ledgers[i] == o2.ledgers[i]
+        assert gpu.breakdown[i] == o2.breakdown[i]
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_large_window_many_tiles(variant):
     """m = 50 (the config 2 / config 5 extreme) over ~20 tiles, recycle included."""
