@@ -92,7 +92,8 @@ def read_traffic(variant, m):
 class Clocks:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+         "power.limit,clocks.mem")   # (power and memory clock: box-to-box context)
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
@@ -127,7 +128,7 @@ class Clocks:
             self.proc.wait(timeout=3)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        sm, smax, reasons, pw, plim, mem = [], [], set(), [], [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -141,11 +142,24 @@ class Clocks:
             for nm, val in zip(names, parts[5:9]):
                 if val.lower() == "active":
                     reasons.add(nm)
+            for lst, val in ((pw, parts[3]), (plim, parts[9] if len(parts) > 9 else ""),
+                             (mem, parts[10] if len(parts) > 10 else "")):
+                try:
+                    lst.append(float(val))
+                except ValueError:
+                    pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
         loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)),
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:
+            out["power_w"] = float(np.median(pw))
+        if plim:
+            out["power_limit_w"] = float(max(plim))
+        if mem:
+            out["mem_mhz"] = float(np.median(mem))
+        return out
 
 
 # --------------------------------------------------------------------- oracle baseline
