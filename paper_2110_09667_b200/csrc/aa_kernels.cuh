@@ -919,6 +919,16 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
   const int vb = p.vb;
 
   K4Head hd{};
+  // K4's run-time scalars come from the previous kernels' reductions and the previous step's
+  // state: thread 0 of every CTA loads them now, so the last CTA's tail has no dependent
+  // global loads (small n: the tail is on the step's critical path)
+  K4Head tail_hd{};
+  double tail_f2 = 0.0, tail_rmin = 0.0;
+  if (OP == OP_K4 && tid == 0 && p.chunk_last && !(p.flags & F_DELETE_ONLY)) {
+    tail_hd = k4_scalars_head(p);
+    tail_f2 = p.red[0];
+    tail_rmin = p.st->rratio_min;
+  }
   if (blockIdx.x == 0) AA_TL(0);
   // tile CTAs: all, or (K4 / K1 pre_cta) all but CTA 0, which only does the factor precompute
   const int pre = (OP == OP_K4 || OP == OP_K1) ? p.pre_cta : 0;
@@ -1620,11 +1630,11 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
     // run-time scalars (the factors were written by CTA 0 from its head)
     if (tid == 0 && p.chunk_last && !(p.flags & F_DELETE_ONLY)) {
       SmallState* st = p.st;
-      hd = k4_scalars_head(p);
+      hd = tail_hd;
       st->last_rkk = hd.rkk;
       const double dfn = sqrt(hd.df2);
       const double ratio = dfn > 0.0 ? hd.rkk / dfn : 0.0;
-      if (ratio < st->rratio_min) st->rratio_min = ratio;
+      if (ratio < tail_rmin) st->rratio_min = ratio;
       if (!(hd.rkk > p.eps_a * dfn)) {   // reading A12: this step's column is dependent
         st->breakdown = 1;
         st->breakdown_count += 1;
@@ -1634,7 +1644,7 @@ __global__ void __launch_bounds__(NT, 1) aa_stream_kernel(const __grid_constant_
         }
       }
       if (!(p.flags & F_EXT_DF)) {
-        st->f2 = p.red[0];
+        st->f2 = tail_f2;
         st->dx2_local = outv[0];
       }
     }

@@ -7,6 +7,19 @@ ns = [int(float(a)) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else [
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 K = 200
 stream = torch.cuda.current_stream()
+torch.manual_seed(9667)   # the same d, b every run
+
+
+def step(s, x, g, xn):
+    """aa_step with the caller's restart policy: a breakdown surfaced at entry
+    (the nudged problem's differences can become collinear) resets the window once"""
+    try:
+        s.step(x, g, xn)
+    except aa.AAError as e:
+        if e.code != 6:
+            raise
+        s.reset()
+        s.step(x, g, xn)
 for n in ns:
     d = torch.rand(n, dtype=torch.float64, device="cuda") * 1.8 - 0.9
     b = torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1
@@ -27,11 +40,11 @@ for n in ns:
         x.zero_()
         s.init(x, torch.addcmul(b, d, x), xn); x, xn = xn, x
         for _ in range(m + 10):
-            b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
+            b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); step(s, x, g, xn); x, xn = xn, x
         torch.cuda.synchronize()
         e0.record()
         for _ in range(K):
-            b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); s.step(x, g, xn); x, xn = xn, x
+            b.mul_(1.0 + 1e-3); torch.addcmul(b, d, x, out=g); step(s, x, g, xn); x, xn = xn, x
         e1.record(); torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / K * 1e3
         out.append(f"{v} {t - tg:6.1f}")
