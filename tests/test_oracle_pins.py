@@ -228,6 +228,35 @@ def test_dcgs2_rscale_keeps_the_factorisation_consistent():
     assert lv == lr
 
 
+def test_dcgs2_verbatim_r_update_is_plus_s():
+    """Pins Alg. 6 l.5 as printed, R_{0:k-2,k-1} += s (reading A3), against a wrong sign, a
+    missing update or a scaled one -- by scale equivariance, not by retyping the formula.
+    Scaling F by 2 scales every dot product, norm and R entry by exactly 2 and leaves Q (so
+    s = Q^T q, from normalised columns) bitwise unchanged: for the verbatim update
+    D = 2 R(F) - R(2F) is then exactly the s added to each column, the consistent update
+    (R += R_kk s) gives D = 0, and the two runs differ by R_rscale - R_verbatim = (R_kk - 1) s
+    = (R_kk - 1) D column by column.  F is scaled by 2^20 first (exact), so R_kk >> 1 and a
+    wrong sign (which would give R_rscale - R_verbatim = -(R_kk + 1) D) is far off."""
+    A = problems.ortho_test_matrix(600, 14, 1e8, seed=4) * 2.0 ** 20
+    Qv, Rv = (lambda st: (st.Q, st.R))(_build("dcgs2", A)[0])
+    Qv2, Rv2 = (lambda st: (st.Q, st.R))(_build("dcgs2", 2.0 * A)[0])
+    Rr, Rr2 = _build("dcgs2", A, dcgs2_rscale=True)[0].R, _build("dcgs2", 2.0 * A, dcgs2_rscale=True)[0].R
+    assert np.array_equal(Qv, Qv2)
+    assert np.array_equal(2.0 * Rr, Rr2)   # the consistent update is scale-equivariant
+    D, E = 2.0 * Rv - Rv2, Rr - Rv
+    checked = 0
+    for j in range(2, 13):   # columns updated by a later reorthogonalisation (m_i > 3)
+        d, e, rkk = D[:j, j], E[:j, j], Rv[j, j]
+        assert rkk == Rr[j, j]
+        col = np.max(np.abs(Rv[:j, j]))
+        if np.max(np.abs(d)) < 1e4 * EPS * col:   # s still at rounding level in this column
+            continue
+        assert np.max(np.abs(e - (rkk - 1.0) * d)) <= 1e-3 * np.max(np.abs(e)), j
+        assert np.max(np.abs(e + (rkk + 1.0) * d)) >= 0.5 * np.max(np.abs(e)), j   # (discriminates)
+        checked += 1
+    assert checked >= 4, checked
+
+
 @pytest.mark.parametrize("kappa", [1e1, 1e3, 1e6, 1e9])
 def test_loss_of_orthogonality_classes(kappa):
     """S:211 with c = 100, n = 500, m = 20: MGS, ICWY <= c eps kappa (P:169, P:189);
