@@ -497,3 +497,37 @@ def test_block_constant_reduction_property():
         rs = aa_variant(Gsmall, np.zeros(40), 5, v, 15, record_loo=False)
         for xb, ys in zip(rb.xs, rs.xs):
             assert np.linalg.norm(xb - np.repeat(ys / sw, w)) <= 1e-12 * np.linalg.norm(xb)
+
+
+def test_loss_of_orthogonality_closed_forms():
+    """||I - Q^T Q||_F on cases with closed forms: two unit columns at
+    angle theta give sqrt(2) |cos theta|; a column of norm 2 gives |1 - 4| = 3; an exactly
+    orthonormal Q (a permutation) gives 0."""
+    from oracle.qr import loss_of_orthogonality
+    for theta in (0.3, 1.0, np.pi / 2):
+        Q = np.zeros((5, 2))
+        Q[0, 0] = 1.0
+        Q[0, 1], Q[1, 1] = np.cos(theta), np.sin(theta)
+        assert abs(loss_of_orthogonality(Q) - np.sqrt(2.0) * abs(np.cos(theta))) <= 4 * EPS
+    assert loss_of_orthogonality(2.0 * np.eye(3)[:, :1]) == 3.0
+    assert loss_of_orthogonality(np.eye(6)[:, [3, 0, 5]]) == 0.0
+
+
+def test_triangular_solves_match_a_library_routine():
+    """The oracle's substitutions (LSP back-substitution, Alg. 2 l.9; ICWY's unit-lower
+    forward solve with T, Alg. 4 l.4) against scipy's LAPACK trsv on random well-conditioned
+    systems, and exactly on an integer unit-lower system with a known solution."""
+    from scipy.linalg import solve_triangular
+    from oracle.qr import back_substitution, forward_substitution_unit_lower
+    rng = np.random.default_rng(11)
+    for k in (1, 2, 7, 20):
+        R = np.triu(rng.standard_normal((k, k))) + 4.0 * np.eye(k)
+        c = rng.standard_normal(k)
+        assert np.allclose(back_substitution(R, c), solve_triangular(R, c, lower=False), rtol=1e-13, atol=1e-14)
+        T = np.tril(rng.standard_normal((k, k)), -1) * 0.3 + np.eye(k)
+        s = rng.standard_normal(k)
+        assert np.allclose(forward_substitution_unit_lower(T, s),
+                           solve_triangular(T, s, lower=True, unit_diagonal=True), rtol=1e-13, atol=1e-14)
+    T = np.array([[1.0, 0, 0], [2.0, 1.0, 0], [-1.0, 3.0, 1.0]])
+    x = np.array([1.0, -2.0, 5.0])
+    assert np.array_equal(forward_substitution_unit_lower(T, T @ x), x)
