@@ -531,3 +531,25 @@ def test_triangular_solves_match_a_library_routine():
     T = np.array([[1.0, 0, 0], [2.0, 1.0, 0], [-1.0, 3.0, 1.0]])
     x = np.array([1.0, -2.0, 5.0])
     assert np.array_equal(forward_substitution_unit_lower(T, T @ x), x)
+
+
+def test_sharded_reducer_is_exact_on_integers_and_splits_like_spec():
+    """The simulated shards: on integer data every partial and total is
+    exact, so p shards give the plain sums bitwise for every reduction shape; the shard
+    bounds put the remainder rows on the leading ranks."""
+    rng = np.random.default_rng(5)
+    n, k = 1003, 6
+    A = rng.integers(-50, 50, size=(n, k)).astype(np.float64)
+    B = rng.integers(-50, 50, size=(n, 2)).astype(np.float64)
+    v = rng.integers(-50, 50, size=n).astype(np.float64)
+    exact_dot = int(sum(int(a) * int(b) for a, b in zip(v, A[:, 0])))
+    for p in (1, 2, 3, 7, 1003):
+        red = Reducer(p)
+        assert red.dot(v, A[:, 0]) == exact_dot
+        assert np.array_equal(red.matT_vec(A, v), A.T @ v)
+        assert np.array_equal(red.matT_mat(A, B), A.T @ B)
+        assert np.array_equal(red.gram(A), A.T @ A)
+        bounds = list(red._bounds(n))
+        lens = [hi - lo for lo, hi in bounds]
+        assert bounds[0][0] == 0 and bounds[-1][1] == n and sum(lens) == n
+        assert max(lens) - min(lens) <= 1 and lens == sorted(lens, reverse=True)
