@@ -290,8 +290,11 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   bool k1_two = false;
   // (the Gram instances too when they fit: m = 10 K1 0.70 -> 0.72, m = 20 0.76 -> 0.77 of peak)
   if (OP == OP_K1 && nin < 20 && regs <= 128)
-    // K1 with few columns: keep two CTAs per SM (16 warps hide the rotation chain)
-    k1_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, 2, c->max_tr_blocks, &tr, &stages) && tr >= (skew ? 252 : 256);
+    // K1 with few columns: keep two CTAs per SM (16 warps hide the rotation chain); the Gram
+    // instances with a third stage when it still fits (ICWY m = 5: K1 2.46 -> 2.27 ms, m = 10
+    // equal; profiles/r02/icwy_smallm_tiles.txt)
+    k1_two = choose_tile(nin, skew, vec_only, 104 * 1024, 2, G > 0 ? 3 : 2, c->max_tr_blocks, &tr, &stages) &&
+             tr >= (skew ? 252 : 256);
   // CGS-2's K2a (phase B dots the y that phase A just produced, so a tile's two phases
   // serialise): two CTAs per SM overlap them -- the tallest tile, up to 1024 rows, whose
   // 2-stage ring lets two CTAs share an SM (sweeps: m = 20 256 rows, K2 5.34 -> 5.05 ms;
