@@ -306,14 +306,16 @@ int launch_inst(aa_ctx* c, KParams& p, size_t /*unused*/, int cls) {
   // rows when few columns let a 2-stage ring fit (m = 5 / 10: K2 3-6 % faster; m >= 20 falls
   // back to 512 rows by itself); K1 and K4 keep 512
   const bool tall = vec_only || OP == OP_K2_ICWY || OP == OP_K2_DCGS2 || OP == OP_K2B_CGS2;
-  // the fused-dot K1 (NCW 2..3, no Gram) frees its stage right after the row pass: a third
-  // stage in flight pays (m = 10: K1 3.86 -> 3.67 ms, profiles/r02/k1_tiles.txt)
-  // (K1 with the ICWY Gram: up to 6 stages of its 252-row tiles measured slower -- m = 10
-  // 0.69 -> 0.50, m = 20 0.77 -> 0.59 of peak -- so it keeps 2)
-  const int k1_max_stages = (OP == OP_K1 && G == 0 && NCW >= 2 && NCW <= 3) ? 3 : 2;
+  // K1 keeps 2 stages here: the fused-dot form at m = 10 took 3 on an earlier build and box
+  // (K1 3.74 -> 3.67 ms, profiles/r02/k1_tiles.txt), but on the final build 2 measured faster
+  // in both repetitions (3.54 -> 3.37 ms, profiles/r02/tiles_final_ab.txt); the ICWY Gram K1
+  // with up to 6 stages of 252-row tiles was slower (m = 10 0.69 -> 0.50, m = 20 0.77 -> 0.59)
+  const int k1_max_stages = 2;
   if (!k1_two && !k2a_two)
     choose_tile(nin, skew, vec_only, 220 * 1024, 2, k1_max_stages, tall ? 1024 : c->max_tr_blocks, &tr, &stages);
-  if (OP != OP_K1) {
+  // (MGS's one-axpy-one-dot K2 keeps 2: with 4 its 1024-row tiles measured 8 % slower,
+  // m = 10 K2 4.63 -> 4.24 ms, m = 20 9.80 -> 9.02 ms, profiles/r02/tiles_final_ab.txt)
+  if (OP != OP_K1 && OP != OP_K2_MGS) {
     const size_t sb = align_up((size_t)nin * tr, 16) * sizeof(double);
     const size_t budget = (regs <= 128 && 2 * sb <= 104 * 1024) ? 104 * 1024 : 0;
     if (budget) stages = (int)std::max<size_t>(2, std::min<size_t>(4, budget / sb));
