@@ -116,11 +116,12 @@ def test_ragged_sizes_and_windows(n, m, variant):
         assert np.isfinite(a).all()
 
 
-@pytest.mark.parametrize("m", [3, 8, 9, 17, 34, 41, 58, 64])
+@pytest.mark.parametrize("m", [3, 8, 9, 17, 34, 41, 45, 50, 58, 64])
 def test_icwy_gram_column_forms(m):
     """ICWY's recycle K1 carries the Gram in two forms: Delta f and f_i as
     Gram columns k, k+1 when they fit the k columns' 8-column groups (k mod 8 in 1..6:
-    m = 3, 34, 58) and the block multi-dot beside the Gram otherwise (k mod 8 in {0, 7}:
+    m = 3, 34, 45, 50, 58; at 5..7 groups the blocks split over two warp groups) and the block
+    multi-dot beside the Gram otherwise (k mod 8 in {0, 7}:
     m = 8, 9, 17, 41, 64); both against O2 through start-up and 8 recycle steps."""
     n = 20003
     # spectrum in [-0.5, 0.99): slow enough that m = 64 reaches recycle unconverged, and the
