@@ -206,7 +206,9 @@ int aa_step(aa_handle_t h, const double* x_i, const double* gx_i, double* x_next
  * previous aa_step_host call of this handle returned (kept on the device; AA_ERR_STATE if
  * there was none since aa_init, or an aa_step came in between), so a host-side loop
  * x -> G(x) uploads only G(x_i) per iteration.  At n_local >= 4M rows the copies go in row
- * chunks overlapped with K1 (uploads) and K4 (downloads). */
+ * chunks overlapped with K1 (uploads) and K4 (downloads).  Like aa_step it returns
+ * AA_ERR_BREAKDOWN at entry (nranks == 1) before touching anything, so after aa_reset the
+ * same call -- x_i_host = NULL included -- can be repeated. */
 int aa_step_host(aa_handle_t h, const double* x_i_host, const double* gx_i_host,
                  double* x_next_host);
 

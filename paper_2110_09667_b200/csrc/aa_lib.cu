@@ -1321,6 +1321,9 @@ int aa_step_host(aa_handle_t h, const double* x_i, const double* gx_i, double* x
   RET_IF(check_handle(h));
   if (!h->inited) return AA_ERR_STATE;
   if (!gx_i || !x_next) return AA_ERR_ARG;
+  // the breakdown poll of aa_step, before anything changes: after aa_reset the caller retries
+  // the same call (x_i = NULL still finds its device copy)
+  if (h->nranks == 1 && *reinterpret_cast<volatile int*>(h->bd_host)) return AA_ERR_BREAKDOWN;
   // x_i = NULL: the x_{i+1} the previous aa_step_host returned, still on the device (the
   // staging buffers swap roles; only G(x_i) crosses PCIe on the way in)
   if (!x_i && !h->hxn_valid) return AA_ERR_STATE;

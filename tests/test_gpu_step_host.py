@@ -98,3 +98,33 @@ def test_step_host_reuses_device_x(n):
         outs.append(xs)
     for a, c in zip(*outs):
         assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("n", [4097, 5_000_003])
+def test_step_host_breakdown_then_restart_reuses_device_x(n):
+    """The restart policy through aa_step_host (aa.h BREAKDOWN): G(x) = x + 1 makes
+    every Delta f exactly 0, so the first AA step breaks down and degrades to x_{i+1} = G(x_i);
+    the next aa_step_host refuses at entry (AA_ERR_BREAKDOWN) without consuming its inputs;
+    after aa_reset the same call with x_i = NULL finds the device copy of x_{i+1} and again
+    returns G(x_i) -- all exact in fp64."""
+    stream = torch.cuda.current_stream()
+    s = aa.AndersonSolver(n, 3, "dcgs2", stream=stream)
+    one = torch.ones(n, dtype=torch.float64)
+    x0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    x1 = torch.empty_like(x0)
+    s.init(x0, one.cuda(), x1)                       # x1 = G(0) = 1
+    xh = x1.cpu().pin_memory()
+    gh = torch.empty(n, dtype=torch.float64).pin_memory()
+    oh = torch.empty(n, dtype=torch.float64).pin_memory()
+    torch.add(xh, one, out=gh)
+    s.step_host(xh, gh, oh)                          # Delta f = 0: breakdown, x2 = G(x1) = 2
+    assert torch.equal(oh, torch.full_like(oh, 2.0))
+    xh, oh = oh, xh
+    torch.add(xh, one, out=gh)
+    with pytest.raises(aa.AAError) as ei:
+        s.step_host(None, gh, oh)
+    assert ei.value.code == aa.AA_ERR_BREAKDOWN
+    s.reset()
+    s.step_host(None, gh, oh)                        # reuses x2 on the device: x3 = G(x2) = 3
+    assert torch.equal(oh, torch.full_like(oh, 3.0))
+    s.close()
