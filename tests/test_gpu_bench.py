@@ -43,3 +43,21 @@ def test_gpu_arm_json_line():
     assert L["gpu_launches"] == 3 * L["steps"]   # DCGS-2: K1, K2, K4 per step
     assert "sm_mhz" in L["clocks"] and "reasons" in L["clocks"]
     assert {f"{v}_m{m}" for v in ("dcgs2", "icwy", "cgs2", "mgs", "icwy_small") for m in (5, 10, 20, 50)} <= set(L["sweep"])
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_gpu_arm_json_line_torchrun():
+    """The driver's N > 1 launch (torchrun, one rank per GPU): rank 0 prints one line with the
+    whole-job value, the max-over-ranks timing and the per-exchange latency curve."""
+    world = min(torch.cuda.device_count(), 4)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29561", os.path.join(ROOT, "bench.py"),
+                        "--gpus", str(world), "--n-local", "2097152", "--steps", "3", "--warmup", "3", "--no-sweep"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    L = json.loads(lines[0])
+    assert L["n_gpus"] == world and L["scaling"] == "weak"
+    assert "exchange_latency" in L and L["e2e"]["value"] > 0 and L["gpu_launches"] == 3 * L["steps"]
+    assert all(v["fused_us"] > 0 and v["nccl_us"] > 0 for v in L["exchange_latency"].values())
